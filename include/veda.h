@@ -1,0 +1,187 @@
+/*
+ * veda.h -- C ABI of the B200 (sm_100a) hot path of Veda (arXiv 2605.30325):
+ * distilled tile-sparse self-attention for video DiTs.
+ *
+ * The path (Alg. 2, followed by Eq. 2):
+ *   veda_tile_permute   head-aware 3D tiling
+ *   veda_tile_score     TripPool + phi_q/phi_k + S_pred    (Eqs. 5-6)
+ *   veda_select_topk    exactly-k kept key tiles per row
+ *   veda_sparse_attn_fwd tile-skipping attention
+ *   veda_tile_unpermute  back to token order
+ *
+ * Conventions for every call
+ *   - Pointers are DEVICE pointers unless marked "host".  bf16 tensors are passed
+ *     as uint16_t bit patterns.  All device pointers must be 16-byte aligned.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls only
+ *     enqueue work and return; they never synchronise, allocate or free device
+ *     memory, and keep no pointer after returning.  Host arrays are read during
+ *     the call only.  The caller owns every buffer (workspace sizes come from the
+ *     *_workspace helpers).
+ *   - Errors are returned as veda_status; nothing is printed, thrown or aborted.
+ *     veda_last_error() gives a thread-local detail string for the last failure.
+ *     Faults inside a kernel surface later on the stream as CUDA errors.
+ *   - Supported: B = p_t*p_h*p_w in {64, 128}; d in {64, 128}; 1 <= k <= n_tiles;
+ *     Hh <= 1024 heads per call.  Device must be sm_100 (B200).
+ *
+ * Layouts (Hh = heads in the call; N = T*H*W; N_T = n_tiles; MW = B/32)
+ *   token tensor   x[h][n][c] at x + h*head_stride + n*token_stride + c (elements)
+ *   tiled tensor   [Hh][N_T][B][d] bf16, tile-contiguous (B*d*2 bytes per tile)
+ *   tile_count     [Hh][N_T] int32  real tokens per tile
+ *   slot_mask      [Hh][N_T][MW] uint32, bit b of a tile set iff slot b is real
+ *   scores         [Hh][N_T][N_T] fp32
+ *   idx            [Hh][N_T][k] int32, kept key tiles of each query tile, ascending
+ */
+#ifndef VEDA_H_
+#define VEDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define VEDA_API __attribute__((visibility("default")))
+#else
+#define VEDA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    VEDA_OK = 0,
+    VEDA_ERR_NULL = 1,       /* required pointer is NULL                          */
+    VEDA_ERR_SHAPE = 2,      /* dimension mismatch / unsupported size             */
+    VEDA_ERR_CONFIG = 3,     /* p_t*p_h*p_w differs across heads or B unsupported */
+    VEDA_ERR_K_RANGE = 4,    /* k outside [1, n_tiles]                            */
+    VEDA_ERR_ALIGN = 5,      /* pointer or stride not 16-byte aligned             */
+    VEDA_ERR_WORKSPACE = 6,  /* workspace too small                               */
+    VEDA_ERR_INDEX = 7,      /* (validation call) bad index list                  */
+    VEDA_ERR_NONFINITE = 8,  /* reserved                                          */
+    VEDA_ERR_CUDA = 9,       /* CUDA runtime / driver error at launch             */
+    VEDA_ERR_ARCH = 10       /* current device is not sm_100                      */
+} veda_status;
+
+/* real latent grid (T, H, W); tokens are flattened raster n = (t*H + h)*W + w
+ * (reading R1) */
+typedef struct { int32_t t, h, w; } veda_latent;
+
+/* per-head tile shape pi_{l,h} = (p_t, p_h, p_w), p_t*p_h*p_w = B (Eq. 8) */
+typedef struct { int32_t pt, ph, pw; } veda_tile_cfg;
+
+/* padded grid shared by all heads of a call (reading R4/R5) */
+typedef struct {
+    int32_t tp, hp, wp;   /* padded extents: each axis ceil-padded to the lcm of its tile extents */
+    int32_t B;            /* tile size                                                           */
+    int32_t n_tiles;      /* N_T = tp*hp*wp / B                                                  */
+    int32_t reserved;
+    int64_t n_pad;        /* tp*hp*wp                                                            */
+} veda_tiled_shape;
+
+/* statistic-aware estimator weights, one set per head (Eq. 6;
+ * DESIGN.md reading R8).  Host struct holding DEVICE fp32 arrays:
+ *   w1 [Hh][d_in][d_hidden], b1 [Hh][d_hidden], w2 [Hh][d_hidden][d_lat], b2 [Hh][d_lat]
+ * for the query side (..q) and the key side (..k).  d_in must be 3*d.
+ * phi(z) = GELU(z w1 + b1) w2 + b2, GELU(x) = x*Phi(x) (erf form). */
+typedef struct {
+    int32_t d_in, d_hidden, d_lat;
+    const float *w1q, *b1q, *w2q, *b2q;
+    const float *w1k, *b1k, *w2k, *b2k;
+} veda_scorer;
+
+/* ---- host helpers ----------------------------------------------------------- */
+
+/* Padded grid of a call.  cfg: host [Hh].  PAPER.md:143-145, 288-294; 61x45x80 with
+ * (4,4,8) gives 64x48x80 = 245,760 tokens. */
+VEDA_API veda_status veda_tiled_shape_of(veda_latent lat, const veda_tile_cfg *cfg, int32_t Hh,
+                                veda_tiled_shape *out /* host */);
+
+/* k = floor((1 - sparsity) * n_tiles + 1/2) clamped to [1, n_tiles] (reading R12). */
+VEDA_API int32_t veda_k_for_sparsity(int32_t n_tiles, double sparsity);
+
+/* Bytes of workspace veda_tile_score needs. */
+VEDA_API veda_status veda_tile_score_workspace(int32_t Hh, int32_t n_tiles, int32_t d,
+                                      const veda_scorer *w /* host */, size_t *bytes /* host */);
+
+/* ---- the five steps of the path ------------------------------------------------ */
+
+/* Step 1: head-aware 3D tiling (Alg. 2; Eq. 8).
+ * Tile i of head h is the box (i_t,i_h,i_w) in raster order of boxes; slot j inside
+ * it is (dt,dh,dw) in raster order, t slowest (readings R2, R3).  Padded slots are
+ * written as +0 (R4).  tile_count / slot_mask may be NULL (skipped).
+ *   x        : token tensor, strides in elements, multiples of 8
+ *   x_tiled  : [Hh][N_T][B][d]                                                        */
+VEDA_API veda_status veda_tile_permute(const uint16_t *x, int64_t head_stride, int64_t token_stride,
+                              veda_latent lat, const veda_tile_cfg *cfg /* host [Hh] */,
+                              int32_t Hh, int32_t d, uint16_t *x_tiled, int32_t *tile_count,
+                              uint32_t *slot_mask, void *stream);
+
+/* Step 2: statistics-aware tile scoring, Alg. 2:
+ *   z = Avg (+) Max (+) Min over each tile's real tokens (Eq. 5; readings R6, R7),
+ *   e = phi(z) per head and side, S_ij = e_q,i . e_k,j / sqrt(d_lat) (Eq. 6),
+ *   S_ij = -inf when key tile j has no real token (R5).
+ * Pooling sums and both GEMMs accumulate in fp64 (reading R17); scores are rounded
+ * once to fp32.  Equals veda_trippool x2 -> veda_project x2 -> veda_pair_scores.
+ *   tile_count, slot_mask : from veda_tile_permute (identical for Q and K)
+ *   scores : [Hh][N_T][N_T] fp32;  workspace : >= veda_tile_score_workspace bytes   */
+VEDA_API veda_status veda_tile_score(const uint16_t *q_tiled, const uint16_t *k_tiled,
+                            const int32_t *tile_count, const uint32_t *slot_mask, int32_t Hh,
+                            int32_t n_tiles, int32_t B, int32_t d, const veda_scorer *w /* host */,
+                            float *scores, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Step 3: per-query-tile top-k (Alg. 2).  Exactly k
+ * key tiles per row: order by (S descending, j ascending), keep the first k, emit
+ * ascending (readings R10, R11, R16: -0.0 == +0.0).  Decided on the fp32 scores.  */
+VEDA_API veda_status veda_select_topk(const float *scores, int32_t Hh, int32_t n_tiles, int32_t k,
+                             int32_t *idx, void *stream);
+
+/* Step 4: tile-skipping attention forward, Eq. 2: for each
+ * (head, query tile i) O_i = softmax(Q~_i K^_i^T * scale) V^_i over the k kept tiles
+ * idx[i]; padded key slots are -inf, padded query rows are written as 0 (R4).
+ * bf16 operands, fp32 accumulation (tcgen05 / TMEM), P rounded to bf16 for P.V,
+ * output bf16 (R15).  softmax_scale <= 0 selects 1/sqrt(d).  lse (natural log,
+ * [Hh][N_T][B] fp32) may be NULL.                                                  */
+VEDA_API veda_status veda_sparse_attn_fwd(const uint16_t *q_tiled, const uint16_t *k_tiled,
+                                 const uint16_t *v_tiled, const int32_t *idx,
+                                 const uint32_t *slot_mask, int32_t Hh, int32_t n_tiles,
+                                 int32_t B, int32_t d, int32_t k, float softmax_scale,
+                                 uint16_t *o_tiled, float *lse, void *stream);
+
+/* Step 5: untiling: o[token] = o_tiled[tile][slot] for every real
+ * slot; padded slots are dropped.                                                    */
+VEDA_API veda_status veda_tile_unpermute(const uint16_t *o_tiled, veda_latent lat,
+                                const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh, int32_t d,
+                                uint16_t *o, int64_t head_stride, int64_t token_stride,
+                                void *stream);
+
+/* ---- sub-steps of veda_tile_score (exported for parity tests and profiling) ---- */
+
+/* TripPool (Eq. 5): z [Hh][N_T][3d] fp32 = Avg | Max | Min over real slots; the Avg
+ * sum is accumulated in fp64 and rounded once.  Empty tiles give z = 0.            */
+VEDA_API veda_status veda_trippool(const uint16_t *x_tiled, const uint32_t *slot_mask, int32_t Hh,
+                          int32_t n_tiles, int32_t B, int32_t d, float *z, void *stream);
+
+/* phi (Eq. 6): e [Hh][N_T][d_lat] fp64 = GELU(z w1 + b1) w2 + b2 with fp64
+ * accumulation.  hidden: fp64 scratch [Hh][N_T][d_hidden].                          */
+VEDA_API veda_status veda_project(const float *z, int32_t Hh, int32_t n_tiles, int32_t d_in,
+                         int32_t d_hidden, int32_t d_lat, const float *w1, const float *b1,
+                         const float *w2, const float *b2, double *hidden, double *e,
+                         void *stream);
+
+/* S_ij = e_q,i . e_k,j / sqrt(d_lat) (fp64 accumulate, fp32 store), -inf for empty
+ * key tiles (tile_count == 0).                                                       */
+VEDA_API veda_status veda_pair_scores(const double *eq, const double *ek, const int32_t *tile_count,
+                             int32_t Hh, int32_t n_tiles, int32_t d_lat, float *scores,
+                             void *stream);
+
+/* ---- diagnostics ------------------------------------------------------------------ */
+VEDA_API const char *veda_status_str(veda_status st);
+VEDA_API const char *veda_last_error(void);
+/* Kernels launched by this library since load (process-wide counter). */
+VEDA_API uint64_t veda_launch_count(void);
+/* VEDA_OK iff the current CUDA device is sm_100 and usable. */
+VEDA_API veda_status veda_check_device(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VEDA_H_ */

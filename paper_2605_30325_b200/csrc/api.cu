@@ -1,0 +1,339 @@
+// api.cu -- the C ABI of libveda (include/veda.h): argument validation, shape helpers,
+// workspace carving and kernel dispatch.  All device work is in permute.cu, score.cu,
+// topk.cu and attn_fwd.cu; nothing here touches data.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace veda {
+
+static thread_local char g_err[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+veda_status fail(veda_status st, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+veda_status check_launch(const char *what)
+{
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return VEDA_OK;
+}
+
+int num_sms()
+{
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cache[dev] == 0) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = n > 0 ? n : 148;
+    }
+    return cache[dev];
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+veda_status make_tmap_bf16(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols,
+                           uint32_t box_rows)
+{
+    auto fn = encode_fn();
+    if (!fn) return fail(VEDA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box,
+                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(VEDA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return VEDA_OK;
+}
+
+namespace {
+
+struct Shape {
+    int Tp, Hp, Wp, B, NT;
+};
+
+veda_status check_arch()
+{
+    static int ok_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(VEDA_ERR_CUDA, "no CUDA device");
+    if (dev == ok_dev) return VEDA_OK;
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return fail(VEDA_ERR_ARCH, "device %d is sm_%d%d; libveda is built for sm_100a", dev, major, minor);
+    ok_dev = dev;
+    return VEDA_OK;
+}
+
+int lcm_int(int a, int b)
+{
+    int x = a, y = b;
+    while (y) { const int t = x % y; x = y; y = t; }
+    return a / x * b;
+}
+
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+veda_status shape_of(veda_latent lat, const veda_tile_cfg *cfg, int Hh, Shape *sh, HeadCfgs *hc)
+{
+    if (!cfg) return fail(VEDA_ERR_NULL, "cfg is NULL");
+    if (Hh < 1 || Hh > kMaxHeads) return fail(VEDA_ERR_SHAPE, "Hh=%d outside [1, %d]", Hh, kMaxHeads);
+    if (lat.t < 1 || lat.h < 1 || lat.w < 1) return fail(VEDA_ERR_SHAPE, "latent must be positive");
+    const int B = cfg[0].pt * cfg[0].ph * cfg[0].pw;
+    int Pt = 1, Ph = 1, Pw = 1;
+    for (int h = 0; h < Hh; ++h) {
+        const veda_tile_cfg c = cfg[h];
+        if (!is_pow2(c.pt) || !is_pow2(c.ph) || !is_pow2(c.pw))
+            return fail(VEDA_ERR_CONFIG, "head %d: tile extents must be powers of two", h);
+        if (c.pt * c.ph * c.pw != B) return fail(VEDA_ERR_CONFIG, "head %d: p_t*p_h*p_w != B=%d", h, B);
+        Pt = lcm_int(Pt, c.pt);
+        Ph = lcm_int(Ph, c.ph);
+        Pw = lcm_int(Pw, c.pw);
+        if (hc) { hc->pt[h] = (uint8_t)c.pt; hc->ph[h] = (uint8_t)c.ph; hc->pw[h] = (uint8_t)c.pw; }
+    }
+    if (B != 64 && B != 128) return fail(VEDA_ERR_CONFIG, "B=%d unsupported (64 or 128)", B);
+    sh->Tp = (lat.t + Pt - 1) / Pt * Pt;
+    sh->Hp = (lat.h + Ph - 1) / Ph * Ph;
+    sh->Wp = (lat.w + Pw - 1) / Pw * Pw;
+    sh->B = B;
+    const int64_t npad = (int64_t)sh->Tp * sh->Hp * sh->Wp;
+    if (npad / B > (1 << 24)) return fail(VEDA_ERR_SHAPE, "too many tiles");
+    sh->NT = (int)(npad / B);
+    if ((int64_t)Hh * sh->NT * B > INT32_MAX) return fail(VEDA_ERR_SHAPE, "Hh*n_pad exceeds 2^31 rows");
+    return VEDA_OK;
+}
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+}  // namespace
+}  // namespace veda
+
+using namespace veda;
+
+extern "C" {
+
+veda_status veda_tiled_shape_of(veda_latent lat, const veda_tile_cfg *cfg, int32_t Hh, veda_tiled_shape *out)
+{
+    if (!out) return fail(VEDA_ERR_NULL, "out is NULL");
+    Shape sh;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, nullptr);
+    if (st != VEDA_OK) return st;
+    out->tp = sh.Tp; out->hp = sh.Hp; out->wp = sh.Wp; out->B = sh.B; out->n_tiles = sh.NT;
+    out->reserved = 0;
+    out->n_pad = (int64_t)sh.Tp * sh.Hp * sh.Wp;
+    return VEDA_OK;
+}
+
+int32_t veda_k_for_sparsity(int32_t n_tiles, double sparsity)
+{
+    double kk = std::floor((1.0 - sparsity) * (double)n_tiles + 0.5);
+    if (kk < 1) kk = 1;
+    if (kk > n_tiles) kk = n_tiles;
+    return (int32_t)kk;
+}
+
+veda_status veda_tile_score_workspace(int32_t Hh, int32_t n_tiles, int32_t d, const veda_scorer *w, size_t *bytes)
+{
+    if (!w || !bytes) return fail(VEDA_ERR_NULL, "scorer or bytes is NULL");
+    if (w->d_in != 3 * d) return fail(VEDA_ERR_SHAPE, "d_in=%d must equal 3*d=%d", w->d_in, 3 * d);
+    if (Hh < 1 || n_tiles < 1 || w->d_hidden < 1 || w->d_lat < 1) return fail(VEDA_ERR_SHAPE, "bad sizes");
+    const size_t rows = (size_t)Hh * n_tiles;
+    size_t b = 0;
+    b += 2 * align256(rows * w->d_in * sizeof(float));      // Zq, Zk
+    b += align256(rows * w->d_hidden * sizeof(double));     // hidden (reused by q and k)
+    b += 2 * align256(rows * w->d_lat * sizeof(double));    // Eq, Ek
+    *bytes = b;
+    return VEDA_OK;
+}
+
+veda_status veda_tile_permute(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
+                              const veda_tile_cfg *cfg, int32_t Hh, int32_t d, uint16_t *x_tiled,
+                              int32_t *tile_count, uint32_t *slot_mask, void *stream)
+{
+    if (!x || !x_tiled) return fail(VEDA_ERR_NULL, "tile_permute: NULL tensor");
+    if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "tile_permute: d=%d unsupported", d);
+    if (!aligned16(x) || !aligned16(x_tiled) || (head_stride % 8) || (token_stride % 8))
+        return fail(VEDA_ERR_ALIGN, "tile_permute: pointers/strides must be 16-byte aligned");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    Shape sh;
+    HeadCfgs hc;
+    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    return launch_tile_permute(x, head_stride, token_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w,
+                               sh.B, sh.NT, d, x_tiled, tile_count, slot_mask, S(stream));
+}
+
+veda_status veda_tile_unpermute(const uint16_t *o_tiled, veda_latent lat, const veda_tile_cfg *cfg, int32_t Hh,
+                                int32_t d, uint16_t *o, int64_t head_stride, int64_t token_stride, void *stream)
+{
+    if (!o || !o_tiled) return fail(VEDA_ERR_NULL, "tile_unpermute: NULL tensor");
+    if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "tile_unpermute: d=%d unsupported", d);
+    if (!aligned16(o) || !aligned16(o_tiled) || (head_stride % 8) || (token_stride % 8))
+        return fail(VEDA_ERR_ALIGN, "tile_unpermute: pointers/strides must be 16-byte aligned");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    Shape sh;
+    HeadCfgs hc;
+    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    return launch_tile_unpermute(o_tiled, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B, sh.NT, d, o,
+                                 head_stride, token_stride, S(stream));
+}
+
+veda_status veda_trippool(const uint16_t *x_tiled, const uint32_t *slot_mask, int32_t Hh, int32_t n_tiles,
+                          int32_t B, int32_t d, float *z, void *stream)
+{
+    if (!x_tiled || !slot_mask || !z) return fail(VEDA_ERR_NULL, "trippool: NULL pointer");
+    if ((B != 64 && B != 128) || (d != 64 && d != 128) || Hh < 1 || n_tiles < 1)
+        return fail(VEDA_ERR_SHAPE, "trippool: unsupported B=%d d=%d", B, d);
+    if (!aligned16(x_tiled)) return fail(VEDA_ERR_ALIGN, "trippool: x_tiled not 16-byte aligned");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    return launch_trippool(x_tiled, slot_mask, Hh, n_tiles, B, d, z, S(stream));
+}
+
+veda_status veda_project(const float *z, int32_t Hh, int32_t n_tiles, int32_t d_in, int32_t d_hidden,
+                         int32_t d_lat, const float *w1, const float *b1, const float *w2, const float *b2,
+                         double *hidden, double *e, void *stream)
+{
+    if (!z || !w1 || !b1 || !w2 || !b2 || !hidden || !e) return fail(VEDA_ERR_NULL, "project: NULL pointer");
+    if (Hh < 1 || n_tiles < 1 || d_in < 1 || d_hidden < 1 || d_lat < 1) return fail(VEDA_ERR_SHAPE, "project: bad sizes");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    return launch_project(z, Hh, n_tiles, d_in, d_hidden, d_lat, w1, b1, w2, b2, hidden, e, S(stream));
+}
+
+veda_status veda_pair_scores(const double *eq, const double *ek, const int32_t *tile_count, int32_t Hh,
+                             int32_t n_tiles, int32_t d_lat, float *scores, void *stream)
+{
+    if (!eq || !ek || !tile_count || !scores) return fail(VEDA_ERR_NULL, "pair_scores: NULL pointer");
+    if (Hh < 1 || n_tiles < 1 || d_lat < 1) return fail(VEDA_ERR_SHAPE, "pair_scores: bad sizes");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    return launch_pair_scores(eq, ek, tile_count, Hh, n_tiles, d_lat, scores, S(stream));
+}
+
+veda_status veda_tile_score(const uint16_t *q_tiled, const uint16_t *k_tiled, const int32_t *tile_count,
+                            const uint32_t *slot_mask, int32_t Hh, int32_t n_tiles, int32_t B, int32_t d,
+                            const veda_scorer *w, float *scores, void *workspace, size_t workspace_bytes,
+                            void *stream)
+{
+    if (!q_tiled || !k_tiled || !tile_count || !slot_mask || !w || !scores || !workspace)
+        return fail(VEDA_ERR_NULL, "tile_score: NULL pointer");
+    if (!w->w1q || !w->b1q || !w->w2q || !w->b2q || !w->w1k || !w->b1k || !w->w2k || !w->b2k)
+        return fail(VEDA_ERR_NULL, "tile_score: NULL scorer weight");
+    size_t need = 0;
+    veda_status st = veda_tile_score_workspace(Hh, n_tiles, d, w, &need);
+    if (st != VEDA_OK) return st;
+    if (workspace_bytes < need) return fail(VEDA_ERR_WORKSPACE, "tile_score: workspace %zu < %zu", workspace_bytes, need);
+    if (!aligned16(workspace)) return fail(VEDA_ERR_ALIGN, "tile_score: workspace not aligned");
+    const size_t rows = (size_t)Hh * n_tiles;
+    char *p = static_cast<char *>(workspace);
+    float *zq = reinterpret_cast<float *>(p); p += align256(rows * w->d_in * sizeof(float));
+    float *zk = reinterpret_cast<float *>(p); p += align256(rows * w->d_in * sizeof(float));
+    double *hid = reinterpret_cast<double *>(p); p += align256(rows * w->d_hidden * sizeof(double));
+    double *eq = reinterpret_cast<double *>(p); p += align256(rows * w->d_lat * sizeof(double));
+    double *ek = reinterpret_cast<double *>(p);
+    if ((st = veda_trippool(q_tiled, slot_mask, Hh, n_tiles, B, d, zq, stream)) != VEDA_OK) return st;
+    if ((st = veda_trippool(k_tiled, slot_mask, Hh, n_tiles, B, d, zk, stream)) != VEDA_OK) return st;
+    if ((st = veda_project(zq, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1q, w->b1q, w->w2q, w->b2q, hid, eq,
+                           stream)) != VEDA_OK)
+        return st;
+    if ((st = veda_project(zk, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1k, w->b1k, w->w2k, w->b2k, hid, ek,
+                           stream)) != VEDA_OK)
+        return st;
+    return veda_pair_scores(eq, ek, tile_count, Hh, n_tiles, w->d_lat, scores, stream);
+}
+
+veda_status veda_select_topk(const float *scores, int32_t Hh, int32_t n_tiles, int32_t k, int32_t *idx, void *stream)
+{
+    if (!scores || !idx) return fail(VEDA_ERR_NULL, "select_topk: NULL pointer");
+    if (Hh < 1 || n_tiles < 1) return fail(VEDA_ERR_SHAPE, "select_topk: bad sizes");
+    if (k < 1 || k > n_tiles) return fail(VEDA_ERR_K_RANGE, "select_topk: k=%d outside [1, %d]", k, n_tiles);
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    return launch_topk(scores, Hh, n_tiles, k, idx, S(stream));
+}
+
+veda_status veda_sparse_attn_fwd(const uint16_t *q_tiled, const uint16_t *k_tiled, const uint16_t *v_tiled,
+                                 const int32_t *idx, const uint32_t *slot_mask, int32_t Hh, int32_t n_tiles,
+                                 int32_t B, int32_t d, int32_t k, float softmax_scale, uint16_t *o_tiled,
+                                 float *lse, void *stream)
+{
+    if (!q_tiled || !k_tiled || !v_tiled || !idx || !slot_mask || !o_tiled)
+        return fail(VEDA_ERR_NULL, "sparse_attn_fwd: NULL pointer");
+    if (Hh < 1 || n_tiles < 1 || (int64_t)Hh * n_tiles * B > INT32_MAX)
+        return fail(VEDA_ERR_SHAPE, "sparse_attn_fwd: bad sizes");
+    if (k < 1 || k > n_tiles) return fail(VEDA_ERR_K_RANGE, "sparse_attn_fwd: k=%d outside [1, %d]", k, n_tiles);
+    if (!aligned16(q_tiled) || !aligned16(k_tiled) || !aligned16(v_tiled) || !aligned16(o_tiled))
+        return fail(VEDA_ERR_ALIGN, "sparse_attn_fwd: tensors must be 16-byte aligned");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)d);
+    return launch_sparse_attn(q_tiled, k_tiled, v_tiled, idx, slot_mask, Hh, n_tiles, B, d, k, scale, o_tiled, lse,
+                              S(stream));
+}
+
+const char *veda_status_str(veda_status st)
+{
+    switch (st) {
+    case VEDA_OK: return "VEDA_OK";
+    case VEDA_ERR_NULL: return "VEDA_ERR_NULL";
+    case VEDA_ERR_SHAPE: return "VEDA_ERR_SHAPE";
+    case VEDA_ERR_CONFIG: return "VEDA_ERR_CONFIG";
+    case VEDA_ERR_K_RANGE: return "VEDA_ERR_K_RANGE";
+    case VEDA_ERR_ALIGN: return "VEDA_ERR_ALIGN";
+    case VEDA_ERR_WORKSPACE: return "VEDA_ERR_WORKSPACE";
+    case VEDA_ERR_INDEX: return "VEDA_ERR_INDEX";
+    case VEDA_ERR_NONFINITE: return "VEDA_ERR_NONFINITE";
+    case VEDA_ERR_CUDA: return "VEDA_ERR_CUDA";
+    case VEDA_ERR_ARCH: return "VEDA_ERR_ARCH";
+    }
+    return "VEDA_ERR_UNKNOWN";
+}
+
+const char *veda_last_error(void) { return g_err; }
+
+uint64_t veda_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+veda_status veda_check_device(void) { return check_arch(); }
+
+}  // extern "C"

@@ -1,0 +1,422 @@
+// attn_fwd.cu -- tile-skipping FlashAttention forward for sm_100a (B200).
+//
+// Computes Eq. 2 of the paper: for every (head h, query tile i)
+//     O_i = softmax(Q~_i K^_i^T * scale) V^_i,   K^_i / V^_i = concat of the k kept tiles
+// visiting ONLY the kept key tiles named by idx[h][i][:] (producer
+// fetches "only the selected non-contiguous key/value tiles" into a circular buffer).
+//
+// B200 design:
+//  * persistent, one CTA per SM, 384 threads = 3 warpgroups:
+//      warp 0      TMA producer: Q tiles and the kept K/V tiles -> SMEM ring (SWIZZLE_128B)
+//      warp 1      MMA issuer (one thread): tcgen05.mma, S = Q K^T (SS) and O += P V (TS)
+//      warps 2-3   idle (warpgroup 0 gives its registers away with setmaxnreg)
+//      warps 4-11  two softmax warpgroups ("slots"), one query tile each, one row per thread
+//  * each slot owns 256 TMEM columns: S (fp32, 128 cols; P aliases its first B/2 columns
+//    as packed bf16) and O (fp32, D cols).  The two slots work on different query
+//    tiles with independent kept lists, so one slot's softmax overlaps the other's MMAs.
+//  * online softmax in the log2 domain with lazy rescaling: O (in TMEM) is rescaled
+//    only when a row max grows by more than 8 (2^8 head-room in fp32/bf16).
+//  * padded key slots (slot_mask bit clear) get -inf; padded query rows are written 0.
+//  * ordering: the commit after S_{t} = Q K_t^T also covers the previous O += P_{t-1} V,
+//    so when softmax sees S_t, O is quiescent and may be rescaled in place.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace veda {
+namespace attn {
+using namespace sm100;
+
+constexpr int NSLOT = 2;
+constexpr int NTHREADS = 128 + 128 * NSLOT;
+constexpr int REGS_CTRL = 64;      // setmaxnreg budget of warpgroup 0 (producer / MMA)
+constexpr int REGS_SOFTMAX = 224;  // ... and of each softmax warpgroup (40 + 2*232 <= 512 per SMSP)
+constexpr uint32_t TMEM_COLS = 512;
+
+struct Params {
+    const int32_t *idx;
+    const uint32_t *slot_mask;
+    uint16_t *out;
+    float *lse;
+    int NT, k, total_units;
+    float scale_log2;
+};
+
+template <int B, int D>
+struct Geo {
+    static constexpr int QCHUNK = 128 * 128;         // one 64-col chunk of the 128-row Q buffer
+    static constexpr int Q_BYTES = QCHUNK * (D / 64);
+    static constexpr int KCHUNK = B * 128;           // one 64-col chunk of a B-row K/V tile
+    static constexpr int TILE_BYTES = KCHUNK * (D / 64);
+    static constexpr int NST_FIT = (200 * 1024 - NSLOT * Q_BYTES) / TILE_BYTES;
+    static constexpr int NST = NST_FIT > 8 ? 8 : NST_FIT;
+    static constexpr int MW = B / 32;
+    static constexpr int NBAR = 2 * NST + 5 * NSLOT;
+    static constexpr int SMEM = NSLOT * Q_BYTES + NST * TILE_BYTES + NBAR * 8 + 16 + 1024;
+    static_assert(NST >= 2, "ring too shallow");
+};
+
+__device__ __forceinline__ float u2f(uint32_t u) { return __uint_as_float(u); }
+__device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
+
+template <int B, int D>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
+                           const __grid_constant__ CUtensorMap tmK,
+                           const __grid_constant__ CUtensorMap tmV, const Params p)
+{
+    using G = Geo<B, D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                ~uintptr_t(1023));
+    const uint32_t sQ = smem_u32(smem);
+    const uint32_t sRing = sQ + NSLOT * G::Q_BYTES;
+    const uint32_t sBar = sRing + G::NST * G::TILE_BYTES;
+    uint32_t *tmem_slot =
+        reinterpret_cast<uint32_t *>(smem + NSLOT * G::Q_BYTES + G::NST * G::TILE_BYTES + G::NBAR * 8);
+    // barrier addresses
+#define RING_FULL(i) (sBar + 8u * (i))
+#define RING_EMPTY(i) (sBar + 8u * (G::NST + (i)))
+#define Q_FULL(s) (sBar + 8u * (2 * G::NST + (s)))
+#define Q_EMPTY(s) (sBar + 8u * (2 * G::NST + NSLOT + (s)))
+#define S_FULL(s) (sBar + 8u * (2 * G::NST + 2 * NSLOT + (s)))
+#define P_FULL(s) (sBar + 8u * (2 * G::NST + 3 * NSLOT + (s)))
+#define O_FULL(s) (sBar + 8u * (2 * G::NST + 4 * NSLOT + (s)))
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (B < 128) {  // rows B..127 of the M=128 Q operand are never loaded: keep them zero
+        uint4 *q4 = reinterpret_cast<uint4 *>(smem);
+        for (int i = threadIdx.x; i < NSLOT * G::Q_BYTES / 16; i += NTHREADS) q4[i] = make_uint4(0, 0, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < G::NST; ++i) {
+            mbar_init(RING_FULL(i), 1);
+            mbar_init(RING_EMPTY(i), 1);
+        }
+        for (int s = 0; s < NSLOT; ++s) {
+            mbar_init(Q_FULL(s), 1);
+            mbar_init(Q_EMPTY(s), 1);
+            mbar_init(S_FULL(s), 1);
+            mbar_init(P_FULL(s), 128);
+            mbar_init(O_FULL(s), 1);
+        }
+        fence_barrier_init();
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+    }
+    if (warp == 1) {
+        tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+
+    const int NT = p.NT, K = p.k, total = p.total_units;
+    const int gslots = gridDim.x * NSLOT;
+    const int rounds = (total + gslots - 1) / gslots;
+    // unit u = h*NT + i; consecutive CTAs/slots take consecutive query tiles of one head (L2 reuse)
+#define UNIT_OF(r, s) ((r) * gslots + blockIdx.x * NSLOT + (s))
+
+    if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS_CTRL));
+    if (warp == 0) {
+        // ============================ TMA producer ============================
+        if (lane == 0) {
+            uint32_t stage = 0, ph = 0;
+            uint32_t qe_bits = 0;  // per-slot phase bits of Q_EMPTY
+            for (int r = 0; r < rounds; ++r) {
+                int u[NSLOT], hh[NSLOT], jv[NSLOT];
+                bool act[NSLOT];
+                const int32_t *il[NSLOT];
+#pragma unroll
+                for (int s = 0; s < NSLOT; ++s) {
+                    u[s] = UNIT_OF(r, s);
+                    act[s] = u[s] < total;
+                    hh[s] = act[s] ? u[s] / NT : 0;
+                    il[s] = p.idx + (size_t)(act[s] ? u[s] : 0) * K;
+                }
+#pragma unroll
+                for (int s = 0; s < NSLOT; ++s) {
+                    if (!act[s]) continue;
+                    mbar_wait(Q_EMPTY(s), ((qe_bits >> s) & 1u) ^ 1u);
+                    qe_bits ^= 1u << s;
+                    mbar_expect_tx(Q_FULL(s), B * D * 2);
+#pragma unroll
+                    for (int c = 0; c < D / 64; ++c)
+                        tma_load_2d(sQ + s * G::Q_BYTES + c * G::QCHUNK, &tmQ, c * 64, u[s] * B, Q_FULL(s));
+                }
+                auto load_tile = [&](const CUtensorMap *tm, int h, int j) {
+                    mbar_wait(RING_EMPTY(stage), ph ^ 1);
+                    mbar_expect_tx(RING_FULL(stage), G::TILE_BYTES);
+                    const int row = (h * NT + j) * B;
+#pragma unroll
+                    for (int c = 0; c < D / 64; ++c)
+                        tma_load_2d(sRing + stage * G::TILE_BYTES + c * G::KCHUNK, tm, c * 64, row,
+                                    RING_FULL(stage));
+                    if (++stage == G::NST) { stage = 0; ph ^= 1; }
+                };
+#pragma unroll
+                for (int s = 0; s < NSLOT; ++s)
+                    if (act[s]) { jv[s] = __ldg(il[s]); load_tile(&tmK, hh[s], jv[s]); }
+                for (int t = 0; t < K; ++t) {
+#pragma unroll
+                    for (int s = 0; s < NSLOT; ++s) {
+                        if (!act[s]) continue;
+                        const int jn = (t + 1 < K) ? __ldg(il[s] + t + 1) : 0;
+                        load_tile(&tmV, hh[s], jv[s]);
+                        if (t + 1 < K) { jv[s] = jn; load_tile(&tmK, hh[s], jv[s]); }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ============================ MMA issuer ============================
+        if (lane == 0) {
+            constexpr uint32_t idesc_qk = idesc_bf16_f32(128, B, 0, 0);  // Q, K both K-major
+            constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D, 0, 1);  // P K-major (TMEM), V MN-major
+            uint32_t stage = 0, ph = 0;
+            uint32_t qf_bits = 0, pf_bits = 0;  // per-slot phase bits of Q_FULL / P_FULL
+            for (int r = 0; r < rounds; ++r) {
+                uint32_t act_bits = 0;
+#pragma unroll
+                for (int s = 0; s < NSLOT; ++s) act_bits |= (UNIT_OF(r, s) < total ? 1u : 0u) << s;
+                auto qk = [&](int s, int t) {
+                    if (t == 0) { mbar_wait(Q_FULL(s), (qf_bits >> s) & 1u); qf_bits ^= 1u << s; }
+                    mbar_wait(RING_FULL(stage), ph);
+                    tc_fence_after();
+                    const uint32_t qa = sQ + s * G::Q_BYTES, kb = sRing + stage * G::TILE_BYTES;
+                    const uint32_t tS = tbase + s * 256;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint64_t ad = sdesc_sw128(qa + (kk >> 2) * G::QCHUNK + (kk & 3) * 32, 16, 1024);
+                        const uint64_t bd = sdesc_sw128(kb + (kk >> 2) * G::KCHUNK + (kk & 3) * 32, 16, 1024);
+                        mma_ss(tS, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+                    }
+                    tc_commit(RING_EMPTY(stage));
+                    tc_commit(S_FULL(s));
+                    if (t == K - 1) tc_commit(Q_EMPTY(s));
+                    if (++stage == G::NST) { stage = 0; ph ^= 1; }
+                };
+                auto pv = [&](int s, int t) {
+                    mbar_wait(P_FULL(s), (pf_bits >> s) & 1u);
+                    pf_bits ^= 1u << s;
+                    mbar_wait(RING_FULL(stage), ph);
+                    tc_fence_after();
+                    const uint32_t vb = sRing + stage * G::TILE_BYTES;
+                    const uint32_t tP = tbase + s * 256, tO = tbase + s * 256 + 128;
+#pragma unroll
+                    for (int kk = 0; kk < B / 16; ++kk) {
+                        // V tile as the MN-major B operand: 16 keys = 16 rows of 128 B; the
+                        // second 64-wide chunk of d sits one KCHUNK further (LBO).
+                        const uint64_t bd = sdesc_sw128(vb + kk * 2048, G::KCHUNK, 1024);
+                        mma_ts(tO, tP + kk * 8, bd, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    tc_commit(RING_EMPTY(stage));
+                    if (t == K - 1) tc_commit(O_FULL(s));
+                    if (++stage == G::NST) { stage = 0; ph ^= 1; }
+                };
+                for (int s = 0; s < NSLOT; ++s)
+                    if ((act_bits >> s) & 1u) qk(s, 0);
+                for (int t = 0; t < K; ++t) {
+                    for (int s = 0; s < NSLOT; ++s) {
+                        if (!((act_bits >> s) & 1u)) continue;
+                        pv(s, t);
+                        if (t + 1 < K) qk(s, t + 1);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_SOFTMAX));
+        // ============================ softmax warpgroups ============================
+        const int slot = (warp - 4) >> 2;
+        const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+        const uint32_t tS = tbase + lane_off + slot * 256;
+        const uint32_t tO = tS + 128;
+        const float sl2 = p.scale_log2;
+        uint32_t sf_ph = 0, of_ph = 0;
+        for (int r = 0; r < rounds; ++r) {
+            const int u = UNIT_OF(r, slot);
+            if (u >= total) break;
+            const int h = u / NT;
+            const int32_t *il = p.idx + (size_t)u * K;
+            const uint32_t *mbase = p.slot_mask + (size_t)h * NT * G::MW;
+            float m = -INFINITY, l = 0.f;
+            int jn = __ldg(il);
+            for (int t = 0; t < K; ++t) {
+                uint32_t mk[G::MW];
+#pragma unroll
+                for (int w = 0; w < G::MW; ++w) mk[w] = __ldg(mbase + (size_t)jn * G::MW + w);
+                if (t + 1 < K) jn = __ldg(il + t + 1);
+
+                mbar_wait(S_FULL(slot), sf_ph);
+                sf_ph ^= 1;
+                tc_fence_after();
+                uint32_t sr[B / 32][32];
+#pragma unroll
+                for (int c = 0; c < B / 32; ++c) tmem_ld32(tS + c * 32, sr[c]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < B / 32; ++c) reg_fence(sr[c]);
+
+                bool full = true;
+#pragma unroll
+                for (int w = 0; w < G::MW; ++w) full &= (mk[w] == 0xFFFFFFFFu);
+                if (!full) {
+#pragma unroll
+                    for (int c = 0; c < B / 32; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (!((mk[c] >> i) & 1u)) sr[c][i] = f2u(-INFINITY);
+                }
+                float mx = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < B / 32; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) mx = fmaxf(mx, u2f(sr[c][i]));
+                const float mnew = fmaxf(m, mx * sl2);
+                // lazy rescale: only when some row of this warp grew its max by > 8 (log2 units)
+                float f = 1.f;
+                bool rescale = false;
+                if (t == 0) {
+                    m = mnew;
+                } else if (__any_sync(0xFFFFFFFFu, mnew > m + 8.0f)) {
+                    f = (mnew == -INFINITY) ? 1.f : ex2(m - mnew);
+                    rescale = true;
+                    l *= f;
+                    m = mnew;
+                }
+                const float mu = (m == -INFINITY) ? 0.f : m;
+                float ls = 0.f;
+#pragma unroll
+                for (int c2 = 0; c2 < B / 64; ++c2) {
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int c = 2 * c2 + (i >> 4), e = (i & 15) * 2;
+                        const float a = ex2(fmaf(u2f(sr[c][e]), sl2, -mu));
+                        const float b = ex2(fmaf(u2f(sr[c][e + 1]), sl2, -mu));
+                        ls += a + b;
+                        pk[i] = pack_bf16(a, b);
+                    }
+                    tmem_st32(tS + c2 * 32, pk);  // P (bf16 pairs) over S columns already read
+                }
+                if (rescale) {  // O is quiescent (see header); scale it before PV_t accumulates
+#pragma unroll
+                    for (int c = 0; c < D / 32; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_wait_ld();
+                        reg_fence(o);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * f);
+                        tmem_st32(tO + c * 32, o);
+                    }
+                }
+                l += ls;
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(P_FULL(slot));
+            }
+            // ---- epilogue: O / l -> bf16, padded query rows -> 0
+            mbar_wait(O_FULL(slot), of_ph);
+            of_ph ^= 1;
+            tc_fence_after();
+            bool qvalid = false;
+            if (row < B) qvalid = (__ldg(p.slot_mask + (size_t)u * G::MW + (row >> 5)) >> (row & 31)) & 1u;
+            const float inv = (qvalid && l > 0.f) ? 1.f / l : 0.f;
+            uint16_t *orow = p.out + ((size_t)u * B + (row < B ? row : 0)) * D;
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                uint32_t o[32];
+                tmem_ld32(tO + c * 32, o);
+                tmem_wait_ld();
+                reg_fence(o);
+                if (row < B) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(u2f(o[2 * i]) * inv, u2f(o[2 * i + 1]) * inv);
+                    uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+                }
+            }
+            if (p.lse != nullptr && row < B)
+                p.lse[(size_t)u * B + row] = (qvalid && l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+        }
+    }
+#undef UNIT_OF
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tbase, TMEM_COLS);
+    }
+}
+
+template <int B, int D>
+static veda_status launch(const uint16_t *q, const uint16_t *k, const uint16_t *v, const int32_t *idx,
+                          const uint32_t *mask, int Hh, int NT, int kk, float scale, uint16_t *o,
+                          float *lse, cudaStream_t stream)
+{
+    using G = Geo<B, D>;
+    CUtensorMap mq, mk, mv;
+    const uint64_t rows = (uint64_t)Hh * NT * B;
+    veda_status st;
+    if ((st = make_tmap_bf16(&mq, q, rows, D, B)) != VEDA_OK) return st;
+    if ((st = make_tmap_bf16(&mk, k, rows, D, B)) != VEDA_OK) return st;
+    if ((st = make_tmap_bf16(&mv, v, rows, D, B)) != VEDA_OK) return st;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(sparse_attn_fwd_kernel<B, D>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        attr_set = true;
+    }
+    Params p;
+    p.idx = idx;
+    p.slot_mask = mask;
+    p.out = o;
+    p.lse = lse;
+    p.NT = NT;
+    p.k = kk;
+    p.total_units = Hh * NT;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    const int units = Hh * NT;
+    int grid = (units + NSLOT - 1) / NSLOT;
+    const int nsm = num_sms();
+    if (grid > nsm) grid = nsm;
+    sparse_attn_fwd_kernel<B, D><<<grid, NTHREADS, G::SMEM, stream>>>(mq, mk, mv, p);
+    count_launch();
+    return check_launch("sparse_attn_fwd");
+}
+
+}  // namespace attn
+
+veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                               const int32_t *idx, const uint32_t *mask, int Hh, int NT, int B, int d,
+                               int kk, float scale, uint16_t *o, float *lse, cudaStream_t s)
+{
+    if (B == 128 && d == 128) return attn::launch<128, 128>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
+    if (B == 128 && d == 64) return attn::launch<128, 64>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
+    if (B == 64 && d == 128) return attn::launch<64, 128>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
+    if (B == 64 && d == 64) return attn::launch<64, 64>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
+    return fail(VEDA_ERR_CONFIG, "sparse_attn_fwd: unsupported (B=%d, d=%d)", B, d);
+}
+
+}  // namespace veda

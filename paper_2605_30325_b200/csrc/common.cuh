@@ -1,0 +1,52 @@
+// common.cuh -- shared host/device plumbing of libveda (not part of the ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+#include "../../include/veda.h"
+
+namespace veda {
+
+// thread-local detail string for veda_last_error()
+veda_status fail(veda_status st, const char *fmt, ...);
+// count one kernel launch (veda_launch_count)
+void count_launch(uint64_t n = 1);
+// CUDA error after a launch -> VEDA_ERR_CUDA with the runtime's message
+veda_status check_launch(const char *what);
+// number of SMs of the current device (cached per device)
+int num_sms();
+// 2-D bf16 tensor map over a [rows][cols] row-major matrix, SWIZZLE_128B, box {64, box_rows}
+veda_status make_tmap_bf16(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols,
+                           uint32_t box_rows);
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+constexpr int kMaxHeads = 1024;
+
+// per-head tile configuration packed for kernel parameters
+struct HeadCfgs {
+    uint8_t pt[kMaxHeads], ph[kMaxHeads], pw[kMaxHeads];
+};
+
+// launchers (defined in the per-kernel .cu files)
+veda_status launch_tile_permute(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfgs &cf, int Hh,
+                                int Tp, int Hp, int Wp, int T, int H, int W, int B, int NT, int d,
+                                uint16_t *xt, int32_t *cnt, uint32_t *mask, cudaStream_t s);
+veda_status launch_tile_unpermute(const uint16_t *xt, const HeadCfgs &cf, int Hh, int Tp, int Hp,
+                                  int Wp, int T, int H, int W, int B, int NT, int d, uint16_t *x,
+                                  int64_t hs, int64_t ts, cudaStream_t s);
+veda_status launch_trippool(const uint16_t *xt, const uint32_t *mask, int Hh, int NT, int B, int d,
+                            float *z, cudaStream_t s);
+veda_status launch_project(const float *z, int Hh, int NT, int din, int dh, int dl, const float *w1,
+                           const float *b1, const float *w2, const float *b2, double *hidden,
+                           double *e, cudaStream_t s);
+veda_status launch_pair_scores(const double *eq, const double *ek, const int32_t *cnt, int Hh, int NT,
+                               int dl, float *scores, cudaStream_t s);
+veda_status launch_topk(const float *scores, int Hh, int NT, int k, int32_t *idx, cudaStream_t s);
+veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                               const int32_t *idx, const uint32_t *mask, int Hh, int NT, int B, int d,
+                               int kk, float scale, uint16_t *o, float *lse, cudaStream_t s);
+
+}  // namespace veda

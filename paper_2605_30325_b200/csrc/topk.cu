@@ -1,0 +1,131 @@
+// topk.cu -- per-query-tile exact top-k selection (step a5 of the path).
+//
+// PAPER.md:146-149 (exactly k kept key tiles per query tile), PAPER.md:280 ("retain the
+// k highest-scoring key tiles for each query tile"), Alg. 2 line 697.  Readings R10/R11/
+// R16: exactly k; among equal scores the lower key-tile index wins; output ascending;
+// -0.0 == +0.0.
+//
+// One CTA (256 threads) per row.  Scores become order-preserving uint32 keys in smem;
+// a 4-pass 8-bit MSB radix select finds the k-th largest key T and how many keys equal
+// to T must be taken; a final pass in index order emits {key > T} plus the first
+// `need` keys == T, compacted with warp ballots -- so the output is ascending by
+// construction and identical to "sort by (S desc, j asc), take k, sort by j".
+#include "common.cuh"
+
+namespace veda {
+namespace {
+
+__device__ __forceinline__ uint32_t order_key(float f)
+{
+    uint32_t u = __float_as_uint(f);
+    if (u == 0x80000000u) u = 0u;  // -0 -> +0
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+constexpr int TK_THREADS = 256;
+constexpr int TK_WARPS = TK_THREADS / 32;
+
+__global__ void __launch_bounds__(TK_THREADS) topk_kernel(const float *__restrict__ S, int NT, int k,
+                                                          int32_t *__restrict__ idx)
+{
+    extern __shared__ uint32_t keys[];
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t s_prefix, s_kk;
+    __shared__ uint32_t s_w_eq[TK_WARPS], s_w_sel[TK_WARPS];
+    const int row = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float *s = S + (size_t)row * NT;
+    for (int j = tid; j < NT; j += TK_THREADS) keys[j] = order_key(__ldg(s + j));
+
+    uint32_t prefix = 0, pmask = 0, kk = (uint32_t)k;
+#pragma unroll 1
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        hist[tid] = 0;  // TK_THREADS == 256 bins
+        __syncthreads();
+        for (int j = tid; j < NT; j += TK_THREADS) {
+            const uint32_t key = keys[j];
+            if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // lane l owns bins 255-8l ... 248-8l (descending)
+            uint32_t c[8], tot = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) { c[q] = hist[255 - 8 * lane - q]; tot += c[q]; }
+            uint32_t incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            uint32_t run = incl - tot;  // keys with a larger digit than this lane's first bin
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (run < kk && kk <= run + c[q]) {
+                    s_prefix = prefix | ((uint32_t)(255 - 8 * lane - q) << shift);
+                    s_kk = kk - run;
+                }
+                run += c[q];
+            }
+        }
+        __syncthreads();
+        prefix = s_prefix;
+        kk = s_kk;
+        pmask |= 255u << shift;
+    }
+    const uint32_t T = prefix;  // the k-th largest key; kk keys equal to T are taken
+    uint32_t out_base = 0, eq_base = 0;
+    int32_t *out = idx + (size_t)row * k;
+    for (int base = 0; base < NT; base += TK_THREADS) {
+        const int j = base + tid;
+        const uint32_t key = j < NT ? keys[j] : 0u;
+        const bool gt = j < NT && key > T;
+        const bool eq = j < NT && key == T;
+        const uint32_t beq = __ballot_sync(0xFFFFFFFFu, eq);
+        if (lane == 0) s_w_eq[warp] = __popc(beq);
+        __syncthreads();
+        uint32_t eq_before = eq_base, eq_tot = 0;
+#pragma unroll
+        for (int w = 0; w < TK_WARPS; ++w) {
+            if (w < warp) eq_before += s_w_eq[w];
+            eq_tot += s_w_eq[w];
+        }
+        eq_before += __popc(beq & ((1u << lane) - 1u));
+        const bool sel = gt || (eq && eq_before < kk);
+        const uint32_t bsel = __ballot_sync(0xFFFFFFFFu, sel);
+        if (lane == 0) s_w_sel[warp] = __popc(bsel);
+        __syncthreads();
+        uint32_t pos = out_base, sel_tot = 0;
+#pragma unroll
+        for (int w = 0; w < TK_WARPS; ++w) {
+            if (w < warp) pos += s_w_sel[w];
+            sel_tot += s_w_sel[w];
+        }
+        pos += __popc(bsel & ((1u << lane) - 1u));
+        if (sel) out[pos] = j;
+        out_base += sel_tot;
+        eq_base += eq_tot;
+        __syncthreads();  // s_w_* reused next chunk
+    }
+}
+
+}  // namespace
+
+veda_status launch_topk(const float *scores, int Hh, int NT, int k, int32_t *idx, cudaStream_t s)
+{
+    const size_t smem = (size_t)NT * sizeof(uint32_t);
+    if (smem > 200 * 1024) return fail(VEDA_ERR_SHAPE, "select_topk: n_tiles=%d too large", NT);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        attr = smem;
+    }
+    topk_kernel<<<Hh * NT, TK_THREADS, smem, s>>>(scores, NT, k, idx);
+    count_launch();
+    return check_launch("select_topk");
+}
+
+}  // namespace veda

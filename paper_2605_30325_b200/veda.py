@@ -1,0 +1,349 @@
+"""Python binding of libveda (include/veda.h): argument marshalling only.
+
+Every step of the path runs in the CUDA kernels of libveda.so; this module only
+checks tensor properties, allocates outputs with torch (device memory), and passes
+raw pointers and the current CUDA stream through ctypes.  There is no CPU or
+PyTorch fallback: if the library or a B200 is missing, calls raise.
+
+Names follow the C ABI:  tile_permute, tile_score (trippool / project /
+pair_scores), select_topk, sparse_attn_fwd, tile_unpermute, plus the composed
+``sparse_attention`` (the five steps in order, Alg. 2 + Eq. 2).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libveda.so")
+
+VEDA_STATUS = ["VEDA_OK", "VEDA_ERR_NULL", "VEDA_ERR_SHAPE", "VEDA_ERR_CONFIG", "VEDA_ERR_K_RANGE",
+               "VEDA_ERR_ALIGN", "VEDA_ERR_WORKSPACE", "VEDA_ERR_INDEX", "VEDA_ERR_NONFINITE",
+               "VEDA_ERR_CUDA", "VEDA_ERR_ARCH"]
+
+EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_workspace", "veda_tile_permute",
+           "veda_tile_score", "veda_select_topk", "veda_sparse_attn_fwd", "veda_tile_unpermute",
+           "veda_trippool", "veda_project", "veda_pair_scores", "veda_status_str", "veda_last_error",
+           "veda_launch_count", "veda_check_device"]
+
+
+class VedaError(RuntimeError):
+    pass
+
+
+class Latent(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_int32), ("h", ctypes.c_int32), ("w", ctypes.c_int32)]
+
+
+class TileCfg(ctypes.Structure):
+    _fields_ = [("pt", ctypes.c_int32), ("ph", ctypes.c_int32), ("pw", ctypes.c_int32)]
+
+
+class TiledShape(ctypes.Structure):
+    _fields_ = [("tp", ctypes.c_int32), ("hp", ctypes.c_int32), ("wp", ctypes.c_int32), ("B", ctypes.c_int32),
+                ("n_tiles", ctypes.c_int32), ("reserved", ctypes.c_int32), ("n_pad", ctypes.c_int64)]
+
+
+class Scorer(ctypes.Structure):
+    _fields_ = [("d_in", ctypes.c_int32), ("d_hidden", ctypes.c_int32), ("d_lat", ctypes.c_int32)] + [
+        (n, ctypes.c_void_p) for n in ("w1q", "b1q", "w2q", "b2q", "w1k", "b1k", "w2k", "b2k")]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libveda.so and declare signatures.  Raises if the library is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise VedaError(f"{path} not built; run `python -m paper_2605_30325_b200.build`")
+    lib = ctypes.CDLL(path)
+    P, i32, i64, f32, f64, sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float,
+                                 ctypes.c_double, ctypes.c_size_t)
+    sig = {
+        "veda_tiled_shape_of": ([Latent, P, i32, P], i32),
+        "veda_k_for_sparsity": ([i32, f64], i32),
+        "veda_tile_score_workspace": ([i32, i32, i32, P, P], i32),
+        "veda_tile_permute": ([P, i64, i64, Latent, P, i32, i32, P, P, P, P], i32),
+        "veda_tile_score": ([P, P, P, P, i32, i32, i32, i32, P, P, P, sz, P], i32),
+        "veda_select_topk": ([P, i32, i32, i32, P, P], i32),
+        "veda_sparse_attn_fwd": ([P, P, P, P, P, i32, i32, i32, i32, i32, f32, P, P, P], i32),
+        "veda_tile_unpermute": ([P, Latent, P, i32, i32, P, i64, i64, P], i32),
+        "veda_trippool": ([P, P, i32, i32, i32, i32, P, P], i32),
+        "veda_project": ([P, i32, i32, i32, i32, i32, P, P, P, P, P, P, P], i32),
+        "veda_pair_scores": ([P, P, P, i32, i32, i32, P, P], i32),
+        "veda_status_str": ([i32], ctypes.c_char_p),
+        "veda_last_error": ([], ctypes.c_char_p),
+        "veda_launch_count": ([], ctypes.c_uint64),
+        "veda_check_device": ([], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        lib = load()
+        raise VedaError(f"{what}: {VEDA_STATUS[st] if st < len(VEDA_STATUS) else st}: "
+                        f"{lib.veda_last_error().decode()}")
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _cfg_array(cfgs, Hh):
+    cfgs = [tuple(c) for c in cfgs]
+    if len(cfgs) == 1 and Hh > 1:
+        cfgs = cfgs * Hh
+    if len(cfgs) != Hh:
+        raise VedaError(f"{len(cfgs)} tile configs for {Hh} heads")
+    arr = (TileCfg * Hh)(*[TileCfg(*c) for c in cfgs])
+    return arr
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise VedaError("libveda takes CUDA tensors (no CPU fallback)")
+
+
+def launch_count() -> int:
+    return int(load().veda_launch_count())
+
+
+def check_device():
+    _check(load().veda_check_device(), "check_device")
+
+
+@dataclass
+class TiledShapeInfo:
+    tp: int
+    hp: int
+    wp: int
+    B: int
+    n_tiles: int
+    n_pad: int
+
+
+def tiled_shape(lat, cfgs, Hh: int) -> TiledShapeInfo:
+    out = TiledShape()
+    arr = _cfg_array(cfgs, Hh)
+    _check(load().veda_tiled_shape_of(Latent(*lat), arr, Hh, ctypes.byref(out)), "tiled_shape_of")
+    return TiledShapeInfo(out.tp, out.hp, out.wp, out.B, out.n_tiles, out.n_pad)
+
+
+def k_for_sparsity(n_tiles: int, sparsity: float) -> int:
+    return int(load().veda_k_for_sparsity(n_tiles, float(sparsity)))
+
+
+def tile_permute(x: torch.Tensor, lat, cfgs, out=None, meta=True):
+    """x: bf16 [Hh, N, d] view (last stride 1; e.g. x_nhd.transpose(0,1)).
+    Returns (x_tiled [Hh,N_T,B,d], tile_count [Hh,N_T] int32 | None, slot_mask [Hh,N_T,B/32] | None)."""
+    _need_cuda(x)
+    assert x.dtype == torch.bfloat16 and x.dim() == 3 and x.stride(2) == 1
+    Hh, N, d = x.shape
+    sh = tiled_shape(lat, cfgs, Hh)
+    if out is None:
+        out = torch.empty((Hh, sh.n_tiles, sh.B, d), dtype=torch.bfloat16, device=x.device)
+    cnt = mask = None
+    if meta:
+        cnt = torch.empty((Hh, sh.n_tiles), dtype=torch.int32, device=x.device)
+        mask = torch.empty((Hh, sh.n_tiles, sh.B // 32), dtype=torch.int32, device=x.device)
+    st = load().veda_tile_permute(_ptr(x), x.stride(0), x.stride(1), Latent(*lat), _cfg_array(cfgs, Hh), Hh, d,
+                                  _ptr(out), _ptr(cnt), _ptr(mask), _stream())
+    _check(st, "tile_permute")
+    return out, cnt, mask
+
+
+def tile_unpermute(o_tiled: torch.Tensor, lat, cfgs, out=None):
+    """o_tiled [Hh,N_T,B,d] -> out [Hh, N, d] (or into a given [Hh,N,d] view)."""
+    _need_cuda(o_tiled)
+    Hh, NT, B, d = o_tiled.shape
+    N = lat[0] * lat[1] * lat[2]
+    if out is None:
+        out = torch.empty((Hh, N, d), dtype=torch.bfloat16, device=o_tiled.device)
+    assert out.stride(2) == 1
+    st = load().veda_tile_unpermute(_ptr(o_tiled), Latent(*lat), _cfg_array(cfgs, Hh), Hh, d, _ptr(out),
+                                    out.stride(0), out.stride(1), _stream())
+    _check(st, "tile_unpermute")
+    return out
+
+
+def trippool(x_tiled: torch.Tensor, slot_mask: torch.Tensor):
+    _need_cuda(x_tiled, slot_mask)
+    Hh, NT, B, d = x_tiled.shape
+    z = torch.empty((Hh, NT, 3 * d), dtype=torch.float32, device=x_tiled.device)
+    _check(load().veda_trippool(_ptr(x_tiled), _ptr(slot_mask), Hh, NT, B, d, _ptr(z), _stream()), "trippool")
+    return z
+
+
+def project(z: torch.Tensor, w1, b1, w2, b2):
+    _need_cuda(z, w1, b1, w2, b2)
+    Hh, NT, din = z.shape
+    dh, dl = w1.shape[-1], w2.shape[-1]
+    hid = torch.empty((Hh, NT, dh), dtype=torch.float64, device=z.device)
+    e = torch.empty((Hh, NT, dl), dtype=torch.float64, device=z.device)
+    st = load().veda_project(_ptr(z), Hh, NT, din, dh, dl, _ptr(w1), _ptr(b1), _ptr(w2), _ptr(b2), _ptr(hid),
+                             _ptr(e), _stream())
+    _check(st, "project")
+    return e
+
+
+def pair_scores(eq: torch.Tensor, ek: torch.Tensor, tile_count: torch.Tensor):
+    _need_cuda(eq, ek, tile_count)
+    Hh, NT, dl = eq.shape
+    s = torch.empty((Hh, NT, NT), dtype=torch.float32, device=eq.device)
+    st = load().veda_pair_scores(_ptr(eq), _ptr(ek), _ptr(tile_count), Hh, NT, dl, _ptr(s), _stream())
+    _check(st, "pair_scores")
+    return s
+
+
+def make_scorer(w: dict):
+    """ctypes veda_scorer from a dict of CUDA fp32 tensors (synth.scorer_weights layout)."""
+    _need_cuda(*w.values())
+    for v in w.values():
+        assert v.dtype == torch.float32 and v.is_contiguous()
+    din, dh = w["w1q"].shape[-2:]
+    dl = w["w2q"].shape[-1]
+    sc = Scorer(din, dh, dl, *[w[n].data_ptr() for n in ("w1q", "b1q", "w2q", "b2q", "w1k", "b1k", "w2k", "b2k")])
+    return sc
+
+
+class ScoreWorkspace:
+    """Caller-owned workspace for tile_score, sized by veda_tile_score_workspace."""
+
+    def __init__(self, Hh, n_tiles, d, scorer: Scorer, device):
+        n = ctypes.c_size_t(0)
+        _check(load().veda_tile_score_workspace(Hh, n_tiles, d, ctypes.byref(scorer), ctypes.byref(n)),
+               "tile_score_workspace")
+        self.nbytes = n.value
+        self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+
+
+def tile_score(q_tiled, k_tiled, tile_count, slot_mask, scorer: Scorer, workspace: ScoreWorkspace = None,
+               out=None):
+    _need_cuda(q_tiled, k_tiled, tile_count, slot_mask)
+    Hh, NT, B, d = q_tiled.shape
+    if workspace is None:
+        workspace = ScoreWorkspace(Hh, NT, d, scorer, q_tiled.device)
+    if out is None:
+        out = torch.empty((Hh, NT, NT), dtype=torch.float32, device=q_tiled.device)
+    st = load().veda_tile_score(_ptr(q_tiled), _ptr(k_tiled), _ptr(tile_count), _ptr(slot_mask), Hh, NT, B, d,
+                                ctypes.byref(scorer), _ptr(out), _ptr(workspace.buf), workspace.nbytes, _stream())
+    _check(st, "tile_score")
+    return out
+
+
+def select_topk(scores: torch.Tensor, k: int, out=None):
+    _need_cuda(scores)
+    Hh, NT, _ = scores.shape
+    if out is None:
+        out = torch.empty((Hh, NT, k), dtype=torch.int32, device=scores.device)
+    _check(load().veda_select_topk(_ptr(scores), Hh, NT, k, _ptr(out), _stream()), "select_topk")
+    return out
+
+
+def sparse_attn_fwd(q_tiled, k_tiled, v_tiled, idx, slot_mask, scale: float = 0.0, out=None, want_lse=False):
+    _need_cuda(q_tiled, k_tiled, v_tiled, idx, slot_mask)
+    Hh, NT, B, d = q_tiled.shape
+    k = idx.shape[-1]
+    if out is None:
+        out = torch.empty_like(q_tiled)
+    lse = torch.empty((Hh, NT, B), dtype=torch.float32, device=q_tiled.device) if want_lse else None
+    st = load().veda_sparse_attn_fwd(_ptr(q_tiled), _ptr(k_tiled), _ptr(v_tiled), _ptr(idx), _ptr(slot_mask), Hh,
+                                     NT, B, d, k, float(scale), _ptr(out), _ptr(lse), _stream())
+    _check(st, "sparse_attn_fwd")
+    return (out, lse) if want_lse else out
+
+
+class SparseAttention:
+    """The whole hot path with preallocated buffers (one DiT attention layer call).
+
+    q, k, v: bf16 [Hh, N, d] views on the GPU.  Steps (Alg. 2 + Eq. 2):
+    permute Q/K/V -> tile_score -> select_topk -> sparse_attn_fwd -> unpermute.
+    """
+
+    def __init__(self, lat, cfgs, Hh, d, scorer_weights: dict, sparsity=None, k=None, device="cuda"):
+        self.lat, self.cfgs, self.Hh, self.d = tuple(lat), list(cfgs), Hh, d
+        self.shape = tiled_shape(lat, cfgs, Hh)
+        NT, B = self.shape.n_tiles, self.shape.B
+        self.k = k if k is not None else k_for_sparsity(NT, sparsity)
+        self.weights = scorer_weights
+        self.scorer = make_scorer(scorer_weights)
+        dev = torch.device(device)
+        mk = lambda: torch.empty((Hh, NT, B, d), dtype=torch.bfloat16, device=dev)
+        self.qt, self.kt, self.vt, self.ot = mk(), mk(), mk(), mk()
+        self.cnt = torch.empty((Hh, NT), dtype=torch.int32, device=dev)
+        self.mask = torch.empty((Hh, NT, B // 32), dtype=torch.int32, device=dev)
+        self.scores = torch.empty((Hh, NT, NT), dtype=torch.float32, device=dev)
+        self.idx = torch.empty((Hh, NT, self.k), dtype=torch.int32, device=dev)
+        self.ws = ScoreWorkspace(Hh, NT, d, self.scorer, dev)
+
+    def __call__(self, q, k, v, out=None, events=None):
+        """Run the path; ``events`` (optional list of 6 torch.cuda.Event) brackets the steps."""
+        lib, s = load(), _stream()
+        Hh, d, lat = self.Hh, self.d, Latent(*self.lat)
+        cfg = _cfg_array(self.cfgs, Hh)
+        NT, B = self.shape.n_tiles, self.shape.B
+        if out is None:
+            out = torch.empty((Hh, self.lat[0] * self.lat[1] * self.lat[2], d), dtype=torch.bfloat16, device=q.device)
+        ev = events or [None] * 6
+        if ev[0] is not None:
+            ev[0].record()
+        _check(lib.veda_tile_permute(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, _ptr(self.qt),
+                                     _ptr(self.cnt), _ptr(self.mask), s), "tile_permute(q)")
+        _check(lib.veda_tile_permute(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, _ptr(self.kt), None, None,
+                                     s), "tile_permute(k)")
+        _check(lib.veda_tile_permute(_ptr(v), v.stride(0), v.stride(1), lat, cfg, Hh, d, _ptr(self.vt), None, None,
+                                     s), "tile_permute(v)")
+        if ev[1] is not None:
+            ev[1].record()
+        _check(lib.veda_tile_score(_ptr(self.qt), _ptr(self.kt), _ptr(self.cnt), _ptr(self.mask), Hh, NT, B, d,
+                                   ctypes.byref(self.scorer), _ptr(self.scores), _ptr(self.ws.buf), self.ws.nbytes, s),
+               "tile_score")
+        if ev[2] is not None:
+            ev[2].record()
+        _check(lib.veda_select_topk(_ptr(self.scores), Hh, NT, self.k, _ptr(self.idx), s), "select_topk")
+        if ev[3] is not None:
+            ev[3].record()
+        _check(lib.veda_sparse_attn_fwd(_ptr(self.qt), _ptr(self.kt), _ptr(self.vt), _ptr(self.idx), _ptr(self.mask),
+                                        Hh, NT, B, d, self.k, 0.0, _ptr(self.ot), None, s), "sparse_attn_fwd")
+        if ev[4] is not None:
+            ev[4].record()
+        _check(lib.veda_tile_unpermute(_ptr(self.ot), lat, cfg, Hh, d, _ptr(out), out.stride(0), out.stride(1), s),
+               "tile_unpermute")
+        if ev[5] is not None:
+            ev[5].record()
+        return out
+
+    LAUNCHES_PER_CALL = 3 + 2 + 4 + 1 + 1 + 1 + 1  # permute x3, pool x2, mlp 2x2, scores, topk, attn, unpermute
+
+
+def sparse_attention(q, k, v, lat, cfgs, scorer_weights, sparsity=None, k_keep=None):
+    """One-shot convenience: the five steps on [Hh, N, d] bf16 CUDA views -> o [Hh, N, d].
+
+    CPU (pinned) inputs are copied to the current device first and the output is
+    copied back, so the same call measures the end-to-end path."""
+    host = not q.is_cuda
+    if host:
+        dev = torch.device("cuda")
+        q, k, v = (t.to(dev, non_blocking=True) for t in (q, k, v))
+        scorer_weights = {n: w.to(dev, non_blocking=True) for n, w in scorer_weights.items()}
+    Hh, N, d = q.shape
+    path = SparseAttention(lat, cfgs, Hh, d, scorer_weights, sparsity=sparsity, k=k_keep, device=q.device)
+    o = path(q, k, v)
+    return o.cpu() if host else o

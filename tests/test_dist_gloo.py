@@ -1,0 +1,97 @@
+"""Multi-process (world size 2, gloo, CPU) coverage of the N>1 path: head sharding
+(paper_2605_30325_b200/shard.py) and the max-over-ranks timing reduction.  The fp64
+oracle stands in for the CUDA kernels; per-head results of the sharded run must be
+bit-identical to the single-process run (heads are independent)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+LAT = (5, 7, 9)
+CFGS = [(2, 4, 2), (4, 2, 2), (1, 4, 4)]
+D, KK = 8, 3
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _path_for_heads(heads):
+    """The whole path (oracle backend) for the given global heads."""
+    import oracle
+    from paper_2605_30325_b200 import synth
+
+    oracle.build()
+    pre = synth.Preset("dist", LAT, len(CFGS), D, CFGS[0], 0.5)
+    q, k, v = synth.qkv(pre, heads=heads, lat=LAT, d=D, alpha=2.0)
+    w = synth.scorer_weights(pre, heads=heads, d=D, random_bias=True)
+    u = lambda t: t.contiguous().view(torch.int16).numpy().view(np.uint16)
+    cf = [CFGS[h] for h in heads]
+    # the padded grid must be the one of the WHOLE call (all heads), so pass every config
+    # and keep the local heads' rows
+    allq = np.zeros((len(CFGS),) + tuple(q.shape[1:]), np.uint16)
+    allk, allv = allq.copy(), allq.copy()
+    for li, h in enumerate(heads):
+        allq[h], allk[h], allv[h] = u(q[li]), u(k[li]), u(v[li])
+    oq, cnt, mask = oracle.tile_permute(allq, LAT, CFGS)
+    ok_, _, _ = oracle.tile_permute(allk, LAT, CFGS)
+    ov, _, _ = oracle.tile_permute(allv, LAT, CFGS)
+    sel = list(heads)
+    oq, ok_, ov, cnt, mask = oq[sel], ok_[sel], ov[sel], cnt[sel], mask[sel]
+    wn = {n: t.numpy() for n, t in w.items()}
+    eq = oracle.mlp(oracle.trippool(oq, mask), wn["w1q"], wn["b1q"], wn["w2q"], wn["b2q"])
+    ek = oracle.mlp(oracle.trippool(ok_, mask), wn["w1k"], wn["b1k"], wn["w2k"], wn["b2k"])
+    s = oracle.scores(eq, ek, cnt)
+    idx = oracle.topk(s.astype(np.float32).astype(np.float64), KK)
+    o = oracle.sparse_attn(oq, ok_, ov, idx, mask, nthreads=1)
+    return {"idx": idx, "o": o, "s": s}
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_30325_b200 import shard
+
+    heads = shard.head_range(len(CFGS), rank, world)
+    res = _path_for_heads(list(heads))
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (list(heads), res))
+    t = shard.max_over_ranks(float(rank + 1) * 1.5)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "max.npy"), np.array([t]))
+        for hs, r in gathered:
+            for li, h in enumerate(hs):
+                np.save(os.path.join(out_dir, f"idx{h}.npy"), r["idx"][li])
+                np.save(os.path.join(out_dir, f"o{h}.npy"), r["o"][li])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_head_range_partition():
+    from paper_2605_30325_b200 import shard
+
+    for Hh in (1, 3, 12, 24, 40):
+        for G in (1, 2, 4, 8):
+            parts = [list(shard.head_range(Hh, r, G)) for r in range(G)]
+            assert sum(parts, []) == list(range(Hh))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= 1
+    assert [len(shard.head_range(24, r, 8)) for r in range(8)] == [3] * 8
+
+
+def test_gloo_world2_sharded_equals_single(tmp_path):
+    world, port = 2, _free_port()
+    mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    single = _path_for_heads(list(range(len(CFGS))))
+    assert float(np.load(tmp_path / "max.npy")[0]) == 3.0
+    for h in range(len(CFGS)):
+        assert np.array_equal(np.load(tmp_path / f"idx{h}.npy"), single["idx"][h])
+        assert np.array_equal(np.load(tmp_path / f"o{h}.npy"), single["o"][h], equal_nan=True)
