@@ -16,12 +16,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libveda.so")
-OBJ = os.path.join(HERE, "build")
+OUT = os.environ.get("VEDA_LIB_OUT", os.path.join(HERE, "libveda.so"))
+OBJ = os.path.join(HERE, "build" + os.environ.get("VEDA_BUILD_TAG", ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+         "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"] + \
+        os.environ.get("VEDA_NVCC_EXTRA", "").split()
 
 
 def _sources():

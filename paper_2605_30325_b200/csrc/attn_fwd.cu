@@ -34,8 +34,8 @@ using namespace sm100;
 
 constexpr int NSLOT = 2;
 constexpr int NTHREADS = 128 + 128 * NSLOT;
-constexpr int REGS_CTRL = 64;      // setmaxnreg budget of warpgroup 0 (producer / MMA)
-constexpr int REGS_SOFTMAX = 224;  // ... and of each softmax warpgroup (40 + 2*232 <= 512 per SMSP)
+constexpr int REGS_CTRL = 72;      // setmaxnreg budget of warpgroup 0 (producer / MMA)
+constexpr int REGS_SOFTMAX = 216;  // ... and of each softmax warpgroup (72 + 2*216 = 504 per SMSP; 512 deadlocks)
 constexpr uint32_t TMEM_COLS = 512;
 
 struct Params {
@@ -60,6 +60,12 @@ struct Geo {
     static constexpr int SMEM = NSLOT * Q_BYTES + NST * TILE_BYTES + NBAR * 8 + 16 + 1024;
     static_assert(NST >= 2, "ring too shallow");
 };
+
+#ifdef VEDA_ATTN_DEBUG
+#define DBG(...) do { if (blockIdx.x == 0) printf(__VA_ARGS__); } while (0)
+#else
+#define DBG(...) do { } while (0)
+#endif
 
 __device__ __forceinline__ float u2f(uint32_t u) { return __uint_as_float(u); }
 __device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
@@ -128,7 +134,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #define UNIT_OF(r, s) ((r) * gslots + blockIdx.x * NSLOT + (s))
 
     if (warp < 4) {
+#ifndef VEDA_NO_SETMAXNREG
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS_CTRL));
+#endif
+    if (lane == 0) DBG("w%d ctrl start tbase=%x\n", warp, tbase);
     if (warp == 0) {
         // ============================ TMA producer ============================
         if (lane == 0) {
@@ -205,6 +214,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     tc_commit(RING_EMPTY(stage));
                     tc_commit(S_FULL(s));
+                    DBG("mma qk s%d t%d stage%d\n", s, t, stage);
                     if (t == K - 1) tc_commit(Q_EMPTY(s));
                     if (++stage == G::NST) { stage = 0; ph ^= 1; }
                 };
@@ -224,6 +234,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     tc_commit(RING_EMPTY(stage));
                     if (t == K - 1) tc_commit(O_FULL(s));
+                    DBG("mma pv s%d t%d stage%d\n", s, t, stage);
                     if (++stage == G::NST) { stage = 0; ph ^= 1; }
                 };
                 for (int s = 0; s < NSLOT; ++s)
@@ -240,7 +251,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         __syncwarp();
     }
     } else {
+#ifndef VEDA_NO_SETMAXNREG
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_SOFTMAX));
+#endif
+        if (lane == 0) DBG("w%d softmax start\n", warp);
         // ============================ softmax warpgroups ============================
         const int slot = (warp - 4) >> 2;
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
@@ -266,6 +280,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
                 mbar_wait(S_FULL(slot), sf_ph);
                 sf_ph ^= 1;
+                if (lane == 0) DBG("w%d slot%d t%d S ok\n", warp, slot, t);
                 tc_fence_after();
                 uint32_t sr[B / 32][32];
 #pragma unroll
@@ -332,6 +347,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(P_FULL(slot));
+                if (lane == 0) DBG("w%d slot%d t%d P arrive l=%f m=%f\n", warp, slot, t, l, m);
             }
             // ---- epilogue: O / l -> bf16, padded query rows -> 0
             mbar_wait(O_FULL(slot), of_ph);

@@ -4,6 +4,7 @@
 // headers vendored with flashinfer: cute/arch/mma_sm100_desc.hpp).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_bf16.h>
 
 namespace veda { namespace sm100 {
@@ -43,9 +44,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity)
         : "memory");
     return ok != 0;
 }
+// Spin on an mbarrier phase.  A wait that never completes (a pipeline bug) traps
+// after ~2^26 polls instead of hanging the GPU, reporting the barrier it was stuck on.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 {
+    uint32_t spins = 0;
     while (!mbar_try_wait(bar, parity)) {
+        if (++spins == (1u << 26)) {
+#ifdef VEDA_ATTN_DEBUG
+            printf("veda: mbarrier wait timeout block %d thread %d bar 0x%x parity %u\n", blockIdx.x,
+                   threadIdx.x, bar, parity);
+#endif
+            __trap();
+        }
     }
 }
 

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libveda.so")
+LIB_PATH = os.environ.get("VEDA_LIB", os.path.join(_HERE, "libveda.so"))
 
 VEDA_STATUS = ["VEDA_OK", "VEDA_ERR_NULL", "VEDA_ERR_SHAPE", "VEDA_ERR_CONFIG", "VEDA_ERR_K_RANGE",
                "VEDA_ERR_ALIGN", "VEDA_ERR_WORKSPACE", "VEDA_ERR_INDEX", "VEDA_ERR_NONFINITE",
