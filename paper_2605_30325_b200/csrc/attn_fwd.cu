@@ -47,13 +47,17 @@ struct Params {
     float scale_log2;
 };
 
+#ifndef VEDA_RING_BUDGET_KB
+#define VEDA_RING_BUDGET_KB 224  // Q buffers + K/V ring; 227 KB is the per-CTA maximum
+#endif
+
 template <int B, int D>
 struct Geo {
     static constexpr int QCHUNK = 128 * 128;         // one 64-col chunk of the 128-row Q buffer
     static constexpr int Q_BYTES = QCHUNK * (D / 64);
     static constexpr int KCHUNK = B * 128;           // one 64-col chunk of a B-row K/V tile
     static constexpr int TILE_BYTES = KCHUNK * (D / 64);
-    static constexpr int NST_FIT = (200 * 1024 - NSLOT * Q_BYTES) / TILE_BYTES;
+    static constexpr int NST_FIT = (VEDA_RING_BUDGET_KB * 1024 - NSLOT * Q_BYTES) / TILE_BYTES;
     static constexpr int NST = NST_FIT > 8 ? 8 : NST_FIT;
     static constexpr int MW = B / 32;
     static constexpr int NBAR = 2 * NST + 5 * NSLOT;
@@ -66,6 +70,52 @@ struct Geo {
 #else
 #define DBG(...) do { } while (0)
 #endif
+
+// Fraction of exp2 evaluated on the FMA pipe instead of MUFU: one pair in every
+// EMU_EVERY (0 disables).  MUFU.EX2 runs at 16/clk/SM, the same rate at which the
+// tensor core consumes a 128x128 score tile.  Measured (profiles/r01_attn_experiments.md):
+// slower at the current balance (the MMA issue chain, not MUFU, is critical), so off.
+#ifndef VEDA_EMU_EVERY
+#define VEDA_EMU_EVERY 0
+#endif
+constexpr int EMU_EVERY = VEDA_EMU_EVERY;
+
+// 2^x for x <= ~8: 2^x = 2^n * 2^f, n = rint(x) by the 1.5*2^23 trick, f in [-1/2, 1/2],
+// 2^f by a cubic (max rel. error 7.5e-5, far below the bf16 rounding of P, 2^-9).
+__device__ __forceinline__ float ex2_emu(float x)
+{
+    x = fmaxf(x, -125.0f);
+    const float j = x + 12582912.0f;
+    const float f = x - (j - 12582912.0f);
+    float p = fmaf(f, 0.05517162f, 0.24261113f);
+    p = fmaf(p, f, 0.69326097f);
+    p = fmaf(p, f, 0.99992806f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
+}
+
+// packed fp32x2 (sm_100): (d0, d1) = (a0, a1) * b + c
+__device__ __forceinline__ void ffma2_bc(float &d0, float &d1, float a0, float a1, float b, float c)
+{
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %4};\n\t"
+        "mov.b64 rc, {%5, %5};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(a0), "f"(a1), "f"(b), "f"(c));
+}
+// packed fp32x2: (s0, s1) += (a, b)
+__device__ __forceinline__ void fadd2_acc(float &s0, float &s1, float a, float b)
+{
+    asm("{\n\t.reg .b64 ra, rs;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rs, {%0, %1};\n\t"
+        "add.rn.f32x2 rs, rs, ra;\n\t"
+        "mov.b64 {%0, %1}, rs;\n\t}"
+        : "+f"(s0), "+f"(s1)
+        : "f"(a), "f"(b));
+}
 
 __device__ __forceinline__ float u2f(uint32_t u) { return __uint_as_float(u); }
 __device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
@@ -166,6 +216,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 auto load_tile = [&](const CUtensorMap *tm, int h, int j) {
                     mbar_wait(RING_EMPTY(stage), ph ^ 1);
+#ifdef VEDA_DBG_SKIP_V  // timing experiment only: V tiles are not loaded (wrong results)
+                    if (tm == &tmV) {
+                        mbar_expect_tx(RING_FULL(stage), 0);
+                        if (++stage == G::NST) { stage = 0; ph ^= 1; }
+                        return;
+                    }
+#endif
                     mbar_expect_tx(RING_FULL(stage), G::TILE_BYTES);
                     const int row = (h * NT + j) * B;
 #pragma unroll
@@ -299,11 +356,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         for (int i = 0; i < 32; ++i)
                             if (!((mk[c] >> i) & 1u)) sr[c][i] = f2u(-INFINITY);
                 }
-                float mx = -INFINITY;
+                // row max with 8 independent partial maxima (no 128-long dependency chain)
+                float pm[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pm[q] = -INFINITY;
 #pragma unroll
                 for (int c = 0; c < B / 32; ++c)
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) mx = fmaxf(mx, u2f(sr[c][i]));
+                    for (int i = 0; i < 32; ++i) pm[i & 7] = fmaxf(pm[i & 7], u2f(sr[c][i]));
+                const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                       fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
                 const float mnew = fmaxf(m, mx * sl2);
                 // lazy rescale: only when some row of this warp grew its max by > 8 (log2 units)
                 float f = 1.f;
@@ -317,20 +379,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     m = mnew;
                 }
                 const float mu = (m == -INFINITY) ? 0.f : m;
-                float ls = 0.f;
+                float ps[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c2 = 0; c2 < B / 64; ++c2) {
                     uint32_t pk[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int c = 2 * c2 + (i >> 4), e = (i & 15) * 2;
-                        const float a = ex2(fmaf(u2f(sr[c][e]), sl2, -mu));
-                        const float b = ex2(fmaf(u2f(sr[c][e + 1]), sl2, -mu));
-                        ls += a + b;
+                        float x0, x1;
+                        ffma2_bc(x0, x1, u2f(sr[c][e]), u2f(sr[c][e + 1]), sl2, -mu);
+                        float a, b;
+                        if (EMU_EVERY > 0 && (i % EMU_EVERY) == EMU_EVERY - 1) {
+                            a = ex2_emu(x0);  // FMA-pipe polynomial: unloads the MUFU unit
+                            b = ex2_emu(x1);
+                        } else {
+                            a = ex2(x0);
+                            b = ex2(x1);
+                        }
+                        fadd2_acc(ps[(i & 1) * 2], ps[(i & 1) * 2 + 1], a, b);
                         pk[i] = pack_bf16(a, b);
                     }
                     tmem_st32(tS + c2 * 32, pk);  // P (bf16 pairs) over S columns already read
                 }
+                const float ls = (ps[0] + ps[1]) + (ps[2] + ps[3]);
                 if (rescale) {  // O is quiescent (see header); scale it before PV_t accumulates
 #pragma unroll
                     for (int c = 0; c < D / 32; ++c) {
