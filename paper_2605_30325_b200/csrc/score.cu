@@ -9,6 +9,7 @@
 // near-ties < 1e-5, so every reduction here accumulates in fp64 on the FP64 pipe
 // (fp32 x fp32 products are exact in fp64); scores are rounded once to fp32.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -86,80 +87,123 @@ __global__ void __launch_bounds__(128) trippool_kernel(const uint16_t *__restric
 
 // ---------------------------------------------------------------- fp64-accumulating GEMM
 // C[M,N] = A[M,K] . B  with B stored [K][N] (B_TRANS=false) or [N][K] (B_TRANS=true),
-// batched over blockIdx.z.  64x64 CTA tile, BK=16, 256 threads, 4x4 outputs per thread
-// at stride 16 (conflict-free smem reads).  Operands are widened to fp64 in smem.
+// batched over blockIdx.z, operands widened to fp64 in shared memory, fp64 FMA.
+// 128x128 CTA tile, BK = 16, 256 threads, 8x8 outputs per thread laid out as 4x4 pairs
+// (rows qa*32 + ty*2 + {0,1}, cols qb*32 + tx*2 + {0,1}) so every shared-memory read is a
+// 16-byte, bank-conflict-free (or broadcast) load: 8 LDS.128 feed 64 DFMA per k.  The
+// next k-chunk is prefetched into registers while the current one is consumed.
 enum Epi { EPI_GELU_BIAS = 0, EPI_BIAS = 1, EPI_SCORE = 2 };
 
-template <typename TA, typename TB, bool B_TRANS, int EPI>
-__global__ void __launch_bounds__(256) gemm_f64acc_kernel(const TA *__restrict__ A,
-                                                          const TB *__restrict__ Bm,
-                                                          const float *__restrict__ bias,
-                                                          const int32_t *__restrict__ cnt, void *C,
-                                                          int M, int N, int K, int64_t sA, int64_t sB,
-                                                          int64_t sBias, int64_t sC, double inv_den)
+constexpr int GB_M = 128, GB_N = 128, GB_K = 16;
+
+template <typename T>
+__device__ __forceinline__ void load8(const T *p, double (&v)[8], bool ok);
+template <>
+__device__ __forceinline__ void load8<float>(const float *p, double (&v)[8], bool ok)
 {
-    constexpr int BM = 64, BN = 64, BK = 16;
-    __shared__ double As[BK][BM + 1];
-    __shared__ double Bs[BK][BN];
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (ok) {
+        a = __ldg(reinterpret_cast<const float4 *>(p));
+        b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+    }
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <>
+__device__ __forceinline__ void load8<double>(const double *p, double (&v)[8], bool ok)
+{
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double2 x = make_double2(0.0, 0.0);
+        if (ok) x = __ldg(reinterpret_cast<const double2 *>(p) + q);
+        v[2 * q] = x.x;
+        v[2 * q + 1] = x.y;
+    }
+}
+
+template <typename TA, typename TB, bool B_TRANS, int EPI>
+__global__ void __launch_bounds__(256, 1) gemm_f64acc_kernel(const TA *__restrict__ A,
+                                                             const TB *__restrict__ Bm,
+                                                             const float *__restrict__ bias,
+                                                             const int32_t *__restrict__ cnt, void *C,
+                                                             int M, int N, int K, int64_t sA, int64_t sB,
+                                                             int64_t sBias, int64_t sC, double den)
+{
+    __shared__ __align__(16) double As[GB_K][GB_M];
+    __shared__ __align__(16) double Bs[GB_K][GB_N];
     const int z = blockIdx.z;
     A += z * sA;
     Bm += z * sB;
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    double acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-
-    for (int k0 = 0; k0 < K; k0 += BK) {
-        // A tile: 64 rows x 16 k, 4 elements per thread (k fastest for coalescing)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int e = threadIdx.x + q * 256;
-            const int r = e / BK, kk = e % BK;
-            const int gm = m0 + r, gk = k0 + kk;
-            As[kk][r] = (gm < M && gk < K) ? (double)A[(int64_t)gm * K + gk] : 0.0;
-        }
+    const int m0 = blockIdx.y * GB_M, n0 = blockIdx.x * GB_N;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    // global->shared staging: A (and B^T) as 128 rows x 16 k, 8 consecutive k per thread;
+    // B as 16 k x 128 n, 8 consecutive n per thread
+    const int ar = tid >> 1, ak = (tid & 1) * 8;
+    const int bk = tid >> 4, bn = (tid & 15) * 8;
+    double ra[8], rb[8];
+    auto fetch = [&](int k0) {
+        const int gm = m0 + ar;
+        load8<TA>(A + (int64_t)gm * K + k0 + ak, ra, gm < M && k0 + ak < K);
         if (!B_TRANS) {
+            const int gk = k0 + bk;
+            const bool ok = gk < K && n0 + bn < N;
+            if (ok && (N % 8) == 0 && n0 + bn + 8 <= N) {
+                load8<TB>(Bm + (int64_t)gk * N + n0 + bn, rb, true);
+            } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int e = threadIdx.x + q * 256;
-                const int kk = e / BN, c = e % BN;
-                const int gk = k0 + kk, gn = n0 + c;
-                Bs[kk][c] = (gk < K && gn < N) ? (double)Bm[(int64_t)gk * N + gn] : 0.0;
+                for (int q = 0; q < 8; ++q)
+                    rb[q] = (gk < K && n0 + bn + q < N) ? (double)Bm[(int64_t)gk * N + n0 + bn + q] : 0.0;
             }
         } else {
+            const int gn = n0 + ar;
+            load8<TB>(Bm + (int64_t)gn * K + k0 + ak, rb, gn < N && k0 + ak < K);
+        }
+    };
+    auto stash = [&]() {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) As[ak + q][ar] = ra[q];
+        if (!B_TRANS) {
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) *reinterpret_cast<double2 *>(&Bs[bk][bn + q]) = make_double2(rb[q], rb[q + 1]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) Bs[ak + q][ar] = rb[q];
+        }
+    };
+    double acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+
+    fetch(0);
+    for (int k0 = 0; k0 < K; k0 += GB_K) {
+        stash();
+        __syncthreads();
+        if (k0 + GB_K < K) fetch(k0 + GB_K);  // next chunk in flight during the FMAs
+#pragma unroll
+        for (int kk = 0; kk < GB_K; ++kk) {
+            double a[8], b[8];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const int e = threadIdx.x + q * 256;
-                const int c = e / BK, kk = e % BK;
-                const int gk = k0 + kk, gn = n0 + c;
-                Bs[kk][c] = (gk < K && gn < N) ? (double)Bm[(int64_t)gn * K + gk] : 0.0;
+                const double2 x = *reinterpret_cast<const double2 *>(&As[kk][q * 32 + ty * 2]);
+                const double2 y = *reinterpret_cast<const double2 *>(&Bs[kk][q * 32 + tx * 2]);
+                a[2 * q] = x.x; a[2 * q + 1] = x.y;
+                b[2 * q] = y.x; b[2 * q + 1] = y.y;
             }
-        }
-        __syncthreads();
 #pragma unroll
-        for (int kk = 0; kk < BK; ++kk) {
-            double a[4], b[4];
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int gm = m0 + ty + 16 * i;
+    for (int i = 0; i < 8; ++i) {
+        const int gm = m0 + (i >> 1) * 32 + ty * 2 + (i & 1);
         if (gm >= M) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int gn = n0 + tx + 16 * j;
+        for (int j = 0; j < 8; ++j) {
+            const int gn = n0 + (j >> 1) * 32 + tx * 2 + (j & 1);
             if (gn >= N) continue;
             const int64_t o = z * sC + (int64_t)gm * N + gn;
             if (EPI == EPI_GELU_BIAS) {
@@ -169,11 +213,181 @@ __global__ void __launch_bounds__(256) gemm_f64acc_kernel(const TA *__restrict__
                 static_cast<double *>(C)[o] = acc[i][j] + (double)bias[z * sBias + gn];
             } else {
                 const bool empty = cnt[z * (int64_t)N + gn] == 0;
-                static_cast<float *>(C)[o] = empty ? -INFINITY : (float)(acc[i][j] / inv_den);
+                static_cast<float *>(C)[o] = empty ? -INFINITY : (float)(acc[i][j] / den);
             }
         }
     }
 }
+
+// ---------------------------------------------------------------- fp64 tensor-core GEMM
+// Same contract as gemm_f64acc_kernel, on the FP64 tensor cores (DMMA,
+// mma.sync.m8n8k4.f64: exact fp64 products, fp64 accumulation).  128x128 CTA tile,
+// 8 warps as 2 (m) x 4 (n), warp tile 64x32 = 8x4 DMMA tiles, BK = 16 (4 k-steps).
+// Shared tiles are k-major with a 4-double row pad: fragment reads are conflict-free.
+constexpr int DM_PAD = 4;
+
+__device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4], const double (&b)[2])
+{
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+                 "{%0, %1, %2, %3};"
+                 : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+                 : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <typename T>
+__device__ __forceinline__ void load4(const T *p, double (&v)[4], bool ok);
+template <>
+__device__ __forceinline__ void load4<float>(const float *p, double (&v)[4], bool ok)
+{
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok) a = __ldg(reinterpret_cast<const float4 *>(p));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+template <>
+__device__ __forceinline__ void load4<double>(const double *p, double (&v)[4], bool ok)
+{
+    double2 x = make_double2(0.0, 0.0), y = x;
+    if (ok) {
+        x = __ldg(reinterpret_cast<const double2 *>(p));
+        y = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+    }
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
+}
+
+constexpr int DM_THREADS = 512;
+
+template <typename TA, typename TB, bool B_TRANS, int EPI>
+__global__ void __launch_bounds__(DM_THREADS, 1) gemm_dmma_kernel(const TA *__restrict__ A,
+                                                                  const TB *__restrict__ Bm,
+                                                                  const float *__restrict__ bias,
+                                                                  const int32_t *__restrict__ cnt, void *C,
+                                                                  int M, int N, int K, int64_t sA, int64_t sB,
+                                                                  int64_t sBias, int64_t sC, double den)
+{
+    // 128x128 CTA tile, 16 warps as 4 (m) x 4 (n), warp tile 32x32 = 2 x 4 tiles of
+    // mma.m16n8k8.f64, BK = 16.  Shared tiles k-major with a 4-double pad.
+    __shared__ __align__(16) double As[GB_K][GB_M + DM_PAD];
+    __shared__ __align__(16) double Bs[GB_K][GB_N + DM_PAD];
+    const int z = blockIdx.z;
+    A += z * sA;
+    Bm += z * sB;
+    const int m0 = blockIdx.y * GB_M, n0 = blockIdx.x * GB_N;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp >> 2) * 32, wn = (warp & 3) * 32;
+    const int g = lane >> 2, tg = lane & 3;
+    const int ar = tid >> 2, ak = (tid & 3) * 4;   // A / B^T staging: 128 rows x 16 k
+    const int bk = tid >> 5, bn = (tid & 31) * 4;  // B staging: 16 k x 128 n
+    double ra[4], rb[4];
+    auto fetch = [&](int k0) {
+        const int gm = m0 + ar;
+        load4<TA>(A + (int64_t)gm * K + k0 + ak, ra, gm < M && k0 + ak < K);
+        if (!B_TRANS) {
+            const int gk = k0 + bk;
+            if (gk < K && (N % 4) == 0 && n0 + bn + 4 <= N) {
+                load4<TB>(Bm + (int64_t)gk * N + n0 + bn, rb, true);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    rb[q] = (gk < K && n0 + bn + q < N) ? (double)Bm[(int64_t)gk * N + n0 + bn + q] : 0.0;
+            }
+        } else {
+            const int gn = n0 + ar;
+            load4<TB>(Bm + (int64_t)gn * K + k0 + ak, rb, gn < N && k0 + ak < K);
+        }
+    };
+    auto stash = [&]() {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) As[ak + q][ar] = ra[q];
+        if (!B_TRANS) {
+            *reinterpret_cast<double2 *>(&Bs[bk][bn]) = make_double2(rb[0], rb[1]);
+            *reinterpret_cast<double2 *>(&Bs[bk][bn + 2]) = make_double2(rb[2], rb[3]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) Bs[ak + q][ar] = rb[q];
+        }
+    };
+    double acc[2][4][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+    fetch(0);
+    for (int k0 = 0; k0 < K; k0 += GB_K) {
+        stash();
+        __syncthreads();
+        if (k0 + GB_K < K) fetch(k0 + GB_K);
+#pragma unroll
+        for (int ks = 0; ks < GB_K / 8; ++ks) {
+            double a[2][4], b[4][2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int m = wm + i * 16 + g, k = ks * 8 + tg;
+                a[i][0] = As[k][m];
+                a[i][1] = As[k][m + 8];
+                a[i][2] = As[k + 4][m];
+                a[i][3] = As[k + 4][m + 8];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int n = wn + j * 8 + g, k = ks * 8 + tg;
+                b[j][0] = Bs[k][n];
+                b[j][1] = Bs[k + 4][n];
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_16x8x8(acc[i][j], a[i], b[j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int gm = m0 + wm + i * 16 + g + (e >> 1) * 8, gn = n0 + wn + j * 8 + tg * 2 + (e & 1);
+                if (gm >= M || gn >= N) continue;
+                const int64_t o = z * sC + (int64_t)gm * N + gn;
+                const double v = acc[i][j][e];
+                if (EPI == EPI_GELU_BIAS) {
+                    const double x = v + (double)bias[z * sBias + gn];
+                    static_cast<double *>(C)[o] = 0.5 * x * (1.0 + erf(x * 0.70710678118654752440));
+                } else if (EPI == EPI_BIAS) {
+                    static_cast<double *>(C)[o] = v + (double)bias[z * sBias + gn];
+                } else {
+                    const bool empty = cnt[z * (int64_t)N + gn] == 0;
+                    static_cast<float *>(C)[o] = empty ? -INFINITY : (float)(v / den);
+                }
+            }
+}
+
+bool use_dmma()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("VEDA_GEMM");
+        v = (e && e[0] == 's') ? 0 : 1;  // default: FP64 tensor cores
+    }
+    return v == 1;
+}
+
+#define VEDA_GEMM_LAUNCH(TA, TB, TR_, EPI_, grid, ...)                                         \
+    do {                                                                                      \
+        if (use_dmma())                                                                       \
+            gemm_dmma_kernel<TA, TB, TR_, EPI_><<<grid, DM_THREADS, 0, s>>>(__VA_ARGS__);     \
+        else                                                                                  \
+            gemm_f64acc_kernel<TA, TB, TR_, EPI_><<<grid, 256, 0, s>>>(__VA_ARGS__);          \
+    } while (0)
 
 }  // namespace
 
@@ -195,17 +409,16 @@ veda_status launch_project(const float *z, int Hh, int NT, int din, int dh, int 
                            const float *b1, const float *w2, const float *b2, double *hidden,
                            double *e, cudaStream_t s)
 {
-    dim3 g1((dh + 63) / 64, (NT + 63) / 64, Hh);
-    gemm_f64acc_kernel<float, float, false, EPI_GELU_BIAS><<<g1, 256, 0, s>>>(
-        z, w1, b1, nullptr, hidden, NT, dh, din, (int64_t)NT * din, (int64_t)din * dh, dh,
-        (int64_t)NT * dh, 1.0);
+    if ((din % 8) || (dh % 8)) return fail(VEDA_ERR_SHAPE, "project: d_in and d_hidden must be multiples of 8");
+    dim3 g1((dh + GB_N - 1) / GB_N, (NT + GB_M - 1) / GB_M, Hh);
+    VEDA_GEMM_LAUNCH(float, float, false, EPI_GELU_BIAS, g1, z, w1, b1, nullptr, hidden, NT, dh, din,
+                     (int64_t)NT * din, (int64_t)din * dh, dh, (int64_t)NT * dh, 1.0);
     count_launch();
     veda_status st = check_launch("project/layer1");
     if (st != VEDA_OK) return st;
-    dim3 g2((dl + 63) / 64, (NT + 63) / 64, Hh);
-    gemm_f64acc_kernel<double, float, false, EPI_BIAS><<<g2, 256, 0, s>>>(
-        hidden, w2, b2, nullptr, e, NT, dl, dh, (int64_t)NT * dh, (int64_t)dh * dl, dl,
-        (int64_t)NT * dl, 1.0);
+    dim3 g2((dl + GB_N - 1) / GB_N, (NT + GB_M - 1) / GB_M, Hh);
+    VEDA_GEMM_LAUNCH(double, float, false, EPI_BIAS, g2, hidden, w2, b2, nullptr, e, NT, dl, dh,
+                     (int64_t)NT * dh, (int64_t)dh * dl, dl, (int64_t)NT * dl, 1.0);
     count_launch();
     return check_launch("project/layer2");
 }
@@ -213,10 +426,10 @@ veda_status launch_project(const float *z, int Hh, int NT, int din, int dh, int 
 veda_status launch_pair_scores(const double *eq, const double *ek, const int32_t *cnt, int Hh, int NT,
                                int dl, float *scores, cudaStream_t s)
 {
-    dim3 g((NT + 63) / 64, (NT + 63) / 64, Hh);
-    gemm_f64acc_kernel<double, double, true, EPI_SCORE><<<g, 256, 0, s>>>(
-        eq, ek, nullptr, cnt, scores, NT, NT, dl, (int64_t)NT * dl, (int64_t)NT * dl, 0,
-        (int64_t)NT * NT, sqrt((double)dl));
+    if (dl % 8) return fail(VEDA_ERR_SHAPE, "pair_scores: d_lat must be a multiple of 8");
+    dim3 g((NT + GB_N - 1) / GB_N, (NT + GB_M - 1) / GB_M, Hh);
+    VEDA_GEMM_LAUNCH(double, double, true, EPI_SCORE, g, eq, ek, nullptr, cnt, scores, NT, NT, dl,
+                     (int64_t)NT * dl, (int64_t)NT * dl, 0, (int64_t)NT * NT, sqrt((double)dl));
     count_launch();
     return check_launch("pair_scores");
 }
