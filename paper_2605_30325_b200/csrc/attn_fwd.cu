@@ -253,13 +253,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D, 0, 1);  // P K-major (TMEM), V MN-major
             uint32_t stage = 0, ph = 0;
             uint32_t qf_bits = 0, pf_bits = 0;  // per-slot phase bits of Q_FULL / P_FULL
+            uint32_t p_ok = 0;                  // per-slot: P_FULL already observed complete
+            bool ring_ok = false;               // RING_FULL(stage) already observed complete
             for (int r = 0; r < rounds; ++r) {
                 uint32_t act_bits = 0;
 #pragma unroll
                 for (int s = 0; s < NSLOT; ++s) act_bits |= (UNIT_OF(r, s) < total ? 1u : 0u) << s;
+                // After an op's MMAs are queued (the pipe still holds several of them), poll
+                // the barriers the next op will need; a positive poll lets that op skip its
+                // ~150-clk wait, which would otherwise leave the pipe idle.
+                auto poll_after = [&](int s_next_pv) {
+                    ring_ok = mbar_try_wait(RING_FULL(stage), ph);
+                    if (s_next_pv >= 0 && mbar_try_wait(P_FULL(s_next_pv), (pf_bits >> s_next_pv) & 1u))
+                        p_ok |= 1u << s_next_pv;
+                };
                 auto qk = [&](int s, int t) {
                     if (t == 0) { mbar_wait(Q_FULL(s), (qf_bits >> s) & 1u); qf_bits ^= 1u << s; }
-                    mbar_wait(RING_FULL(stage), ph);
+                    if (!ring_ok) mbar_wait(RING_FULL(stage), ph);
                     tc_fence_after();
                     const uint32_t qa = sQ + s * G::Q_BYTES, kb = sRing + stage * G::TILE_BYTES;
                     const uint32_t tS = tbase + s * 256;
@@ -269,16 +279,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const uint64_t bd = sdesc_sw128(kb + (kk >> 2) * G::KCHUNK + (kk & 3) * 32, 16, 1024);
                         mma_ss(tS, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
                     }
-                    tc_commit(RING_EMPTY(stage));
                     tc_commit(S_FULL(s));
                     DBG("mma qk s%d t%d stage%d\n", s, t, stage);
                     if (t == K - 1) tc_commit(Q_EMPTY(s));
                     if (++stage == G::NST) { stage = 0; ph ^= 1; }
+                    // next op: PV of the next active slot (same t) or of slot 0 (next t)
+                    const int sn = (s + 1 < NSLOT && ((act_bits >> (s + 1)) & 1u)) ? s + 1 : 0;
+                    poll_after(sn);
                 };
                 auto pv = [&](int s, int t) {
-                    mbar_wait(P_FULL(s), (pf_bits >> s) & 1u);
+                    if (!((p_ok >> s) & 1u)) mbar_wait(P_FULL(s), (pf_bits >> s) & 1u);
+                    p_ok &= ~(1u << s);
                     pf_bits ^= 1u << s;
-                    mbar_wait(RING_FULL(stage), ph);
+                    if (!ring_ok) mbar_wait(RING_FULL(stage), ph);
                     tc_fence_after();
                     const uint32_t vb = sRing + stage * G::TILE_BYTES;
                     const uint32_t tP = tbase + s * 256, tO = tbase + s * 256 + 128;
@@ -289,13 +302,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const uint64_t bd = sdesc_sw128(vb + kk * 2048, G::KCHUNK, 1024);
                         mma_ts(tO, tP + kk * 8, bd, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
                     }
-                    tc_commit(RING_EMPTY(stage));
                     if (t == K - 1) tc_commit(O_FULL(s));
                     DBG("mma pv s%d t%d stage%d\n", s, t, stage);
                     if (++stage == G::NST) { stage = 0; ph ^= 1; }
+                    poll_after(-1);
                 };
                 for (int s = 0; s < NSLOT; ++s)
                     if ((act_bits >> s) & 1u) qk(s, 0);
+                p_ok = 0;  // polls made before the first P of this round are not meaningful
                 for (int t = 0; t < K; ++t) {
                     for (int s = 0; s < NSLOT; ++s) {
                         if (!((act_bits >> s) & 1u)) continue;
@@ -321,6 +335,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t tO = tS + 128;
         const float sl2 = p.scale_log2;
         uint32_t sf_ph = 0, of_ph = 0;
+        // Ring stage holding K(slot, t) / V(slot, t) of round r.  The producer's load order
+        // is K(s,0) for the A active slots, then per t: V(s,t), K(s,t+1) for each active slot.
+        // The softmax warps release stages (not the MMA thread, which only commits S_FULL).
+        auto stage_of = [&](int r, int t, bool is_v) -> uint32_t {
+            const int A = (UNIT_OF(r, 1) < total) ? 2 : 1;
+            uint32_t g = (uint32_t)r * (2 * NSLOT) * (uint32_t)K;
+            if (!is_v) g += (t == 0) ? slot : A + 2 * A * (t - 1) + 2 * slot + 1;
+            else g += A + 2 * A * t + ((t < K - 1) ? 2 * slot : slot);
+            return g % G::NST;
+        };
         for (int r = 0; r < rounds; ++r) {
             const int u = UNIT_OF(r, slot);
             if (u >= total) break;
@@ -418,12 +442,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(P_FULL(slot));
+                // S_t had landed => QK(t) and every earlier MMA of this slot (PV(t-1)) are
+                // complete: release the ring stages of K(t) and V(t-1) to the producer
+                // (after P is published, off the S -> P critical path)
+                if (quarter == 0 && lane == 0) {
+                    mbar_arrive(RING_EMPTY(stage_of(r, t, false)));
+                    if (t > 0) mbar_arrive(RING_EMPTY(stage_of(r, t - 1, true)));
+                }
                 if (lane == 0) DBG("w%d slot%d t%d P arrive l=%f m=%f\n", warp, slot, t, l, m);
             }
             // ---- epilogue: O / l -> bf16, padded query rows -> 0
             mbar_wait(O_FULL(slot), of_ph);
             of_ph ^= 1;
             tc_fence_after();
+            if (quarter == 0 && lane == 0) mbar_arrive(RING_EMPTY(stage_of(r, K - 1, true)));
             bool qvalid = false;
             if (row < B) qvalid = (__ldg(p.slot_mask + (size_t)u * G::MW + (row >> 5)) >> (row & 31)) & 1u;
             const float inv = (qvalid && l > 0.f) ? 1.f / l : 0.f;
