@@ -45,7 +45,18 @@ struct Params {
     float *lse;
     int NT, k, total_units;
     float scale_log2;
+    unsigned long long *trace;  // VEDA_ATTN_TRACE builds only: per-step clock64 stamps of CTA 0
 };
+
+#ifdef VEDA_ATTN_TRACE
+#define TR(role, step, field)                                                                      \
+    do {                                                                                           \
+        if (blockIdx.x == 0 && (step) < 128 && p.trace)                                            \
+            p.trace[((role) * 128 + (step)) * 8 + (field)] = clock64();                           \
+    } while (0)
+#else
+#define TR(role, step, field) do { } while (0)
+#endif
 
 #ifndef VEDA_RING_BUDGET_KB
 #define VEDA_RING_BUDGET_KB 224  // Q buffers + K/V ring; 227 KB is the per-CTA maximum
@@ -246,75 +257,118 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
         }
         __syncwarp();
+    } else if (warp == 2 || warp == 3) {
+        // ============================ ring-stage release ============================
+        // Warp 2 (slot 0) / warp 3 (slot 1): S_FULL(s) of tile t lands only when QK(s,t)
+        // and every earlier MMA of the issuing thread -- in particular PV(s,t-1) -- are
+        // complete, so the stages of K(s,t) and V(s,t-1) can go back to the producer at
+        // once (O_FULL releases the unit's last V).  Keeping this off the MMA thread and
+        // off the softmax keeps stage hold times short with a 5-stage ring.
+        if (lane == 0) {
+            const int s = warp - 2;
+            uint32_t sf_ph = 0, of_ph = 0;
+            for (int r = 0; r < rounds; ++r) {
+                if (UNIT_OF(r, s) >= total) break;
+                const int A = (UNIT_OF(r, 1) < total) ? 2 : 1;
+                const uint32_t base = (uint32_t)r * (2 * NSLOT) * (uint32_t)K;
+                // global load index of K(s,t) / V(s,t) in the producer's order
+                auto gk = [&](int t) -> uint32_t { return base + (t == 0 ? s : A + 2 * A * (t - 1) + 2 * s + 1); };
+                auto gv = [&](int t) -> uint32_t { return base + A + 2 * A * t + ((t < K - 1) ? 2 * s : s); };
+                for (int t = 0; t < K; ++t) {
+                    mbar_wait(S_FULL(s), sf_ph);
+                    sf_ph ^= 1;
+                    mbar_arrive(RING_EMPTY(gk(t) % G::NST));
+                    if (t > 0) mbar_arrive(RING_EMPTY(gv(t - 1) % G::NST));
+                }
+                mbar_wait(O_FULL(s), of_ph);
+                of_ph ^= 1;
+                mbar_arrive(RING_EMPTY(gv(K - 1) % G::NST));
+            }
+        }
+        __syncwarp();
     } else if (warp == 1) {
         // ============================ MMA issuer ============================
+        // One thread issues, slot by slot, groups [PV(s,t) ; QK(s,t+1)] back to back (the
+        // QK reuses the S/P columns, so it must follow the PV: same thread => in order).
+        // Before a group, the three barriers it needs (P(s,t), the V stage, the next K
+        // stage) are probed in ONE asm block so their latencies overlap; only a barrier
+        // that is not yet complete is then waited on.  Ring stages are released by the
+        // softmax warps; the MMA thread only commits S_FULL (+ Q_EMPTY / O_FULL).
         if (lane == 0) {
             constexpr uint32_t idesc_qk = idesc_bf16_f32(128, B, 0, 0);  // Q, K both K-major
             constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D, 0, 1);  // P K-major (TMEM), V MN-major
             uint32_t stage = 0, ph = 0;
             uint32_t qf_bits = 0, pf_bits = 0;  // per-slot phase bits of Q_FULL / P_FULL
-            uint32_t p_ok = 0;                  // per-slot: P_FULL already observed complete
-            bool ring_ok = false;               // RING_FULL(stage) already observed complete
+            int nqk = 0, npv = 0;
+            (void)nqk; (void)npv;
+            auto next_stage = [&](uint32_t &st, uint32_t &sp) {
+                st = stage;
+                sp = ph;
+                if (++stage == G::NST) { stage = 0; ph ^= 1; }
+            };
+            auto issue_qk = [&](int s, int t, uint32_t st) {
+                const uint32_t qa = sQ + s * G::Q_BYTES, kb = sRing + st * G::TILE_BYTES;
+                const uint32_t tS = tbase + s * 256;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint64_t ad = sdesc_sw128(qa + (kk >> 2) * G::QCHUNK + (kk & 3) * 32, 16, 1024);
+                    const uint64_t bd = sdesc_sw128(kb + (kk >> 2) * G::KCHUNK + (kk & 3) * 32, 16, 1024);
+                    mma_ss(tS, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+                }
+                tc_commit(S_FULL(s));
+                if (t == K - 1) tc_commit(Q_EMPTY(s));
+            };
+            auto issue_pv = [&](int s, int t, uint32_t st) {
+                const uint32_t vb = sRing + st * G::TILE_BYTES;
+                const uint32_t tP = tbase + s * 256, tO = tbase + s * 256 + 128;
+#pragma unroll
+                for (int kk = 0; kk < B / 16; ++kk) {
+                    // V tile as the MN-major B operand: 16 keys = 16 rows of 128 B; the
+                    // second 64-wide chunk of d sits one KCHUNK further (LBO).
+                    const uint64_t bd = sdesc_sw128(vb + kk * 2048, G::KCHUNK, 1024);
+                    mma_ts(tO, tP + kk * 8, bd, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
+                }
+                if (t == K - 1) tc_commit(O_FULL(s));
+            };
             for (int r = 0; r < rounds; ++r) {
                 uint32_t act_bits = 0;
 #pragma unroll
                 for (int s = 0; s < NSLOT; ++s) act_bits |= (UNIT_OF(r, s) < total ? 1u : 0u) << s;
-                // After an op's MMAs are queued (the pipe still holds several of them), poll
-                // the barriers the next op will need; a positive poll lets that op skip its
-                // ~150-clk wait, which would otherwise leave the pipe idle.
-                auto poll_after = [&](int s_next_pv) {
-                    ring_ok = mbar_try_wait(RING_FULL(stage), ph);
-                    if (s_next_pv >= 0 && mbar_try_wait(P_FULL(s_next_pv), (pf_bits >> s_next_pv) & 1u))
-                        p_ok |= 1u << s_next_pv;
-                };
-                auto qk = [&](int s, int t) {
-                    if (t == 0) { mbar_wait(Q_FULL(s), (qf_bits >> s) & 1u); qf_bits ^= 1u << s; }
-                    if (!ring_ok) mbar_wait(RING_FULL(stage), ph);
+                for (int s = 0; s < NSLOT; ++s) {
+                    if (!((act_bits >> s) & 1u)) continue;
+                    uint32_t st, sp;
+                    next_stage(st, sp);
+                    mbar_wait(Q_FULL(s), (qf_bits >> s) & 1u);
+                    qf_bits ^= 1u << s;
+                    mbar_wait(RING_FULL(st), sp);
+                    TR(0, nqk, 0);
                     tc_fence_after();
-                    const uint32_t qa = sQ + s * G::Q_BYTES, kb = sRing + stage * G::TILE_BYTES;
-                    const uint32_t tS = tbase + s * 256;
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint64_t ad = sdesc_sw128(qa + (kk >> 2) * G::QCHUNK + (kk & 3) * 32, 16, 1024);
-                        const uint64_t bd = sdesc_sw128(kb + (kk >> 2) * G::KCHUNK + (kk & 3) * 32, 16, 1024);
-                        mma_ss(tS, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
-                    }
-                    tc_commit(S_FULL(s));
-                    DBG("mma qk s%d t%d stage%d\n", s, t, stage);
-                    if (t == K - 1) tc_commit(Q_EMPTY(s));
-                    if (++stage == G::NST) { stage = 0; ph ^= 1; }
-                    // next op: PV of the next active slot (same t) or of slot 0 (next t)
-                    const int sn = (s + 1 < NSLOT && ((act_bits >> (s + 1)) & 1u)) ? s + 1 : 0;
-                    poll_after(sn);
-                };
-                auto pv = [&](int s, int t) {
-                    if (!((p_ok >> s) & 1u)) mbar_wait(P_FULL(s), (pf_bits >> s) & 1u);
-                    p_ok &= ~(1u << s);
-                    pf_bits ^= 1u << s;
-                    if (!ring_ok) mbar_wait(RING_FULL(stage), ph);
-                    tc_fence_after();
-                    const uint32_t vb = sRing + stage * G::TILE_BYTES;
-                    const uint32_t tP = tbase + s * 256, tO = tbase + s * 256 + 128;
-#pragma unroll
-                    for (int kk = 0; kk < B / 16; ++kk) {
-                        // V tile as the MN-major B operand: 16 keys = 16 rows of 128 B; the
-                        // second 64-wide chunk of d sits one KCHUNK further (LBO).
-                        const uint64_t bd = sdesc_sw128(vb + kk * 2048, G::KCHUNK, 1024);
-                        mma_ts(tO, tP + kk * 8, bd, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
-                    }
-                    if (t == K - 1) tc_commit(O_FULL(s));
-                    DBG("mma pv s%d t%d stage%d\n", s, t, stage);
-                    if (++stage == G::NST) { stage = 0; ph ^= 1; }
-                    poll_after(-1);
-                };
-                for (int s = 0; s < NSLOT; ++s)
-                    if ((act_bits >> s) & 1u) qk(s, 0);
-                p_ok = 0;  // polls made before the first P of this round are not meaningful
+                    issue_qk(s, 0, st);
+                    TR(0, nqk, 2);
+                    ++nqk;
+                }
                 for (int t = 0; t < K; ++t) {
                     for (int s = 0; s < NSLOT; ++s) {
                         if (!((act_bits >> s) & 1u)) continue;
-                        pv(s, t);
-                        if (t + 1 < K) qk(s, t + 1);
+                        const bool more = t + 1 < K;
+                        uint32_t sv, vp, sk = 0, kp = 0;
+                        next_stage(sv, vp);
+                        if (more) next_stage(sk, kp);
+                        const uint32_t pp = (pf_bits >> s) & 1u;
+                        pf_bits ^= 1u << s;
+                        TR(0, npv, 3);
+                        uint32_t okP, okV, okK;
+                        mbar_try_wait3(P_FULL(s), pp, RING_FULL(sv), vp, RING_FULL(more ? sk : sv), more ? kp : vp,
+                                       okP, okV, okK);
+                        if (!okP) mbar_wait(P_FULL(s), pp);
+                        if (!okV) mbar_wait(RING_FULL(sv), vp);
+                        if (more && !okK) mbar_wait(RING_FULL(sk), kp);
+                        TR(0, npv, 4);
+                        tc_fence_after();
+                        issue_pv(s, t, sv);
+                        if (more) issue_qk(s, t + 1, sk);
+                        TR(0, npv, 5);
+                        ++npv;
                     }
                 }
             }
@@ -335,16 +389,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t tO = tS + 128;
         const float sl2 = p.scale_log2;
         uint32_t sf_ph = 0, of_ph = 0;
-        // Ring stage holding K(slot, t) / V(slot, t) of round r.  The producer's load order
-        // is K(s,0) for the A active slots, then per t: V(s,t), K(s,t+1) for each active slot.
-        // The softmax warps release stages (not the MMA thread, which only commits S_FULL).
-        auto stage_of = [&](int r, int t, bool is_v) -> uint32_t {
-            const int A = (UNIT_OF(r, 1) < total) ? 2 : 1;
-            uint32_t g = (uint32_t)r * (2 * NSLOT) * (uint32_t)K;
-            if (!is_v) g += (t == 0) ? slot : A + 2 * A * (t - 1) + 2 * slot + 1;
-            else g += A + 2 * A * t + ((t < K - 1) ? 2 * slot : slot);
-            return g % G::NST;
-        };
         for (int r = 0; r < rounds; ++r) {
             const int u = UNIT_OF(r, slot);
             if (u >= total) break;
@@ -359,7 +403,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int w = 0; w < G::MW; ++w) mk[w] = __ldg(mbase + (size_t)jn * G::MW + w);
                 if (t + 1 < K) jn = __ldg(il + t + 1);
 
+                const int trs = r * K + t, trr = 1 + slot;
+                if (lane == 0 && quarter == 0) TR(trr, trs, 0);
                 mbar_wait(S_FULL(slot), sf_ph);
+                if (lane == 0 && quarter == 0) TR(trr, trs, 1);
                 sf_ph ^= 1;
                 if (lane == 0) DBG("w%d slot%d t%d S ok\n", warp, slot, t);
                 tc_fence_after();
@@ -369,6 +416,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < B / 32; ++c) reg_fence(sr[c]);
+                if (lane == 0 && quarter == 0) TR(trr, trs, 2);
 
                 bool full = true;
 #pragma unroll
@@ -391,6 +439,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                                        fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
                 const float mnew = fmaxf(m, mx * sl2);
+                if (lane == 0 && quarter == 0) TR(trr, trs, 3);
                 // lazy rescale: only when some row of this warp grew its max by > 8 (log2 units)
                 float f = 1.f;
                 bool rescale = false;
@@ -439,23 +488,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                 }
                 l += ls;
+                if (lane == 0 && quarter == 0) TR(trr, trs, 4);
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(P_FULL(slot));
-                // S_t had landed => QK(t) and every earlier MMA of this slot (PV(t-1)) are
-                // complete: release the ring stages of K(t) and V(t-1) to the producer
-                // (after P is published, off the S -> P critical path)
-                if (quarter == 0 && lane == 0) {
-                    mbar_arrive(RING_EMPTY(stage_of(r, t, false)));
-                    if (t > 0) mbar_arrive(RING_EMPTY(stage_of(r, t - 1, true)));
-                }
+                if (lane == 0 && quarter == 0) TR(trr, trs, 5);
                 if (lane == 0) DBG("w%d slot%d t%d P arrive l=%f m=%f\n", warp, slot, t, l, m);
             }
             // ---- epilogue: O / l -> bf16, padded query rows -> 0
             mbar_wait(O_FULL(slot), of_ph);
             of_ph ^= 1;
             tc_fence_after();
-            if (quarter == 0 && lane == 0) mbar_arrive(RING_EMPTY(stage_of(r, K - 1, true)));
             bool qvalid = false;
             if (row < B) qvalid = (__ldg(p.slot_mask + (size_t)u * G::MW + (row >> 5)) >> (row & 31)) & 1u;
             const float inv = (qvalid && l > 0.f) ? 1.f / l : 0.f;
@@ -488,6 +531,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
+static unsigned long long *g_attn_trace = nullptr;
+
 template <int B, int D>
 static veda_status launch(const uint16_t *q, const uint16_t *k, const uint16_t *v, const int32_t *idx,
                           const uint32_t *mask, int Hh, int NT, int kk, float scale, uint16_t *o,
@@ -516,6 +561,7 @@ static veda_status launch(const uint16_t *q, const uint16_t *k, const uint16_t *
     p.k = kk;
     p.total_units = Hh * NT;
     p.scale_log2 = scale * 1.4426950408889634f;
+    p.trace = g_attn_trace;
     const int units = Hh * NT;
     int grid = (units + NSLOT - 1) / NSLOT;
     const int nsm = num_sms();
@@ -526,6 +572,13 @@ static veda_status launch(const uint16_t *q, const uint16_t *k, const uint16_t *
 }
 
 }  // namespace attn
+
+#ifdef VEDA_ATTN_TRACE
+extern "C" __attribute__((visibility("default"))) void veda_dbg_set_attn_trace(void *dev_buf)
+{
+    attn::g_attn_trace = static_cast<unsigned long long *>(dev_buf);
+}
+#endif
 
 veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v,
                                const int32_t *idx, const uint32_t *mask, int Hh, int NT, int B, int d,

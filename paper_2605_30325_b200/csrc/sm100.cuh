@@ -44,6 +44,23 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity)
         : "memory");
     return ok != 0;
 }
+// Probe three mbarrier phases in one asm block: the three TRYWAITs are issued back to
+// back, so their latencies overlap instead of adding up.
+__device__ __forceinline__ void mbar_try_wait3(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1, uint32_t b2,
+                                               uint32_t p2, uint32_t &ok0, uint32_t &ok1, uint32_t &ok2)
+{
+    asm volatile(
+        "{\n\t.reg .pred q0, q1, q2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 q0, [%3], %4;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 q1, [%5], %6;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 q2, [%7], %8;\n\t"
+        "selp.u32 %0, 1, 0, q0;\n\t"
+        "selp.u32 %1, 1, 0, q1;\n\t"
+        "selp.u32 %2, 1, 0, q2;\n\t}"
+        : "=r"(ok0), "=r"(ok1), "=r"(ok2)
+        : "r"(b0), "r"(p0), "r"(b1), "r"(p1), "r"(b2), "r"(p2)
+        : "memory");
+}
 // Spin on an mbarrier phase.  A wait that never completes (a pipeline bug) traps
 // after ~2^26 polls instead of hanging the GPU, reporting the barrier it was stuck on.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)

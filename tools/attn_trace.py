@@ -37,7 +37,7 @@ def main():
     t = tr.view(4, 128, 8).cpu().numpy().astype(np.int64)
     t0 = t[t > 0].min()
     t = np.where(t > 0, t - t0, -1)
-    for role, name in ((0, "slot 0"), (3, "slot 1")):
+    for role, name in ((0, "thread (both slots)"),):
         print(f"MMA warp {name}: qk[n]: wait_ring_start, ring_ok, issued | pv[n]: wait_P_start, P_ok, issued")
         for n in range(a.steps):
             print(f"  n={n:3d} qk {t[role, n, 0]:8d} {t[role, n, 1]:8d} {t[role, n, 2]:8d} | "
