@@ -153,6 +153,23 @@ VEDA_API veda_status veda_tile_unpermute(const uint16_t *o_tiled, veda_latent la
                                 uint16_t *o, int64_t head_stride, int64_t token_stride,
                                 void *stream);
 
+/* ---- fused forms used by the composed path (same results as the unfused calls) ---- */
+
+/* veda_tile_permute + TripPool of the tiled tensor in ONE pass over HBM (the statistics
+ * are taken from the values already in registers): z [Hh][N_T][3d] fp32 as veda_trippool
+ * computes it.  Used for Q and K (Alg. 2).                     */
+VEDA_API veda_status veda_tile_permute_pool(const uint16_t *x, int64_t head_stride, int64_t token_stride,
+                                            veda_latent lat, const veda_tile_cfg *cfg /* host [Hh] */,
+                                            int32_t Hh, int32_t d, uint16_t *x_tiled, int32_t *tile_count,
+                                            uint32_t *slot_mask, float *z, void *stream);
+
+/* veda_tile_score from precomputed TripPool descriptors zq, zk [Hh][N_T][3d] fp32
+ * (phi_q, phi_k and S_pred, Eq. 6); same workspace as veda_tile_score.               */
+VEDA_API veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32_t *tile_count,
+                                            int32_t Hh, int32_t n_tiles, int32_t d,
+                                            const veda_scorer *w /* host */, float *scores, void *workspace,
+                                            size_t workspace_bytes, void *stream);
+
 /* ---- sub-steps of veda_tile_score (exported for parity tests and profiling) ---- */
 
 /* TripPool (Eq. 5): z [Hh][N_T][3d] fp32 = Avg | Max | Min over real slots; the Avg

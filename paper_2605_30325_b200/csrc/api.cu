@@ -185,9 +185,9 @@ veda_status veda_tile_score_workspace(int32_t Hh, int32_t n_tiles, int32_t d, co
     return VEDA_OK;
 }
 
-veda_status veda_tile_permute(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
-                              const veda_tile_cfg *cfg, int32_t Hh, int32_t d, uint16_t *x_tiled,
-                              int32_t *tile_count, uint32_t *slot_mask, void *stream)
+static veda_status tile_permute_impl(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                     const veda_tile_cfg *cfg, int32_t Hh, int32_t d, uint16_t *x_tiled,
+                                     int32_t *tile_count, uint32_t *slot_mask, float *z, void *stream)
 {
     if (!x || !x_tiled) return fail(VEDA_ERR_NULL, "tile_permute: NULL tensor");
     if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "tile_permute: d=%d unsupported", d);
@@ -199,7 +199,23 @@ veda_status veda_tile_permute(const uint16_t *x, int64_t head_stride, int64_t to
     HeadCfgs hc;
     if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
     return launch_tile_permute(x, head_stride, token_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w,
-                               sh.B, sh.NT, d, x_tiled, tile_count, slot_mask, S(stream));
+                               sh.B, sh.NT, d, x_tiled, tile_count, slot_mask, z, S(stream));
+}
+
+veda_status veda_tile_permute(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
+                              const veda_tile_cfg *cfg, int32_t Hh, int32_t d, uint16_t *x_tiled,
+                              int32_t *tile_count, uint32_t *slot_mask, void *stream)
+{
+    return tile_permute_impl(x, head_stride, token_stride, lat, cfg, Hh, d, x_tiled, tile_count, slot_mask, nullptr,
+                             stream);
+}
+
+veda_status veda_tile_permute_pool(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                   const veda_tile_cfg *cfg, int32_t Hh, int32_t d, uint16_t *x_tiled,
+                                   int32_t *tile_count, uint32_t *slot_mask, float *z, void *stream)
+{
+    if (!z) return fail(VEDA_ERR_NULL, "tile_permute_pool: z is NULL");
+    return tile_permute_impl(x, head_stride, token_stride, lat, cfg, Hh, d, x_tiled, tile_count, slot_mask, z, stream);
 }
 
 veda_status veda_tile_unpermute(const uint16_t *o_tiled, veda_latent lat, const veda_tile_cfg *cfg, int32_t Hh,
@@ -274,6 +290,34 @@ veda_status veda_tile_score(const uint16_t *q_tiled, const uint16_t *k_tiled, co
     double *ek = reinterpret_cast<double *>(p);
     if ((st = veda_trippool(q_tiled, slot_mask, Hh, n_tiles, B, d, zq, stream)) != VEDA_OK) return st;
     if ((st = veda_trippool(k_tiled, slot_mask, Hh, n_tiles, B, d, zk, stream)) != VEDA_OK) return st;
+    if ((st = veda_project(zq, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1q, w->b1q, w->w2q, w->b2q, hid, eq,
+                           stream)) != VEDA_OK)
+        return st;
+    if ((st = veda_project(zk, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1k, w->b1k, w->w2k, w->b2k, hid, ek,
+                           stream)) != VEDA_OK)
+        return st;
+    return veda_pair_scores(eq, ek, tile_count, Hh, n_tiles, w->d_lat, scores, stream);
+}
+
+veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32_t *tile_count, int32_t Hh,
+                                   int32_t n_tiles, int32_t d, const veda_scorer *w, float *scores, void *workspace,
+                                   size_t workspace_bytes, void *stream)
+{
+    if (!zq || !zk || !tile_count || !w || !scores || !workspace)
+        return fail(VEDA_ERR_NULL, "tile_score_pooled: NULL pointer");
+    if (!w->w1q || !w->b1q || !w->w2q || !w->b2q || !w->w1k || !w->b1k || !w->w2k || !w->b2k)
+        return fail(VEDA_ERR_NULL, "tile_score_pooled: NULL scorer weight");
+    size_t need = 0;
+    veda_status st = veda_tile_score_workspace(Hh, n_tiles, d, w, &need);
+    if (st != VEDA_OK) return st;
+    if (workspace_bytes < need) return fail(VEDA_ERR_WORKSPACE, "tile_score_pooled: workspace %zu < %zu", workspace_bytes, need);
+    if (!aligned16(workspace)) return fail(VEDA_ERR_ALIGN, "tile_score_pooled: workspace not aligned");
+    const size_t rows = (size_t)Hh * n_tiles;
+    char *p = static_cast<char *>(workspace);
+    p += 2 * align256(rows * w->d_in * sizeof(float));  // Zq/Zk region unused here
+    double *hid = reinterpret_cast<double *>(p); p += align256(rows * w->d_hidden * sizeof(double));
+    double *eq = reinterpret_cast<double *>(p); p += align256(rows * w->d_lat * sizeof(double));
+    double *ek = reinterpret_cast<double *>(p);
     if ((st = veda_project(zq, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1q, w->b1q, w->w2q, w->b2q, hid, eq,
                            stream)) != VEDA_OK)
         return st;

@@ -33,7 +33,7 @@ struct HeadCfgs {
 // launchers (defined in the per-kernel .cu files)
 veda_status launch_tile_permute(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfgs &cf, int Hh,
                                 int Tp, int Hp, int Wp, int T, int H, int W, int B, int NT, int d,
-                                uint16_t *xt, int32_t *cnt, uint32_t *mask, cudaStream_t s);
+                                uint16_t *xt, int32_t *cnt, uint32_t *mask, float *z, cudaStream_t s);
 veda_status launch_tile_unpermute(const uint16_t *xt, const HeadCfgs &cf, int Hh, int Tp, int Hp,
                                   int Wp, int T, int H, int W, int B, int NT, int d, uint16_t *x,
                                   int64_t hs, int64_t ts, cudaStream_t s);

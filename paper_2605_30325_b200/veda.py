@@ -27,7 +27,7 @@ VEDA_STATUS = ["VEDA_OK", "VEDA_ERR_NULL", "VEDA_ERR_SHAPE", "VEDA_ERR_CONFIG", 
 EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_workspace", "veda_tile_permute",
            "veda_tile_score", "veda_select_topk", "veda_sparse_attn_fwd", "veda_tile_unpermute",
            "veda_trippool", "veda_project", "veda_pair_scores", "veda_status_str", "veda_last_error",
-           "veda_launch_count", "veda_check_device"]
+           "veda_launch_count", "veda_check_device", "veda_tile_permute_pool", "veda_tile_score_pooled"]
 
 
 class VedaError(RuntimeError):
@@ -70,6 +70,8 @@ def load(path: str = LIB_PATH):
         "veda_k_for_sparsity": ([i32, f64], i32),
         "veda_tile_score_workspace": ([i32, i32, i32, P, P], i32),
         "veda_tile_permute": ([P, i64, i64, Latent, P, i32, i32, P, P, P, P], i32),
+        "veda_tile_permute_pool": ([P, i64, i64, Latent, P, i32, i32, P, P, P, P, P], i32),
+        "veda_tile_score_pooled": ([P, P, P, i32, i32, i32, P, P, P, sz, P], i32),
         "veda_tile_score": ([P, P, P, P, i32, i32, i32, i32, P, P, P, sz, P], i32),
         "veda_select_topk": ([P, i32, i32, i32, P, P], i32),
         "veda_sparse_attn_fwd": ([P, P, P, P, P, i32, i32, i32, i32, i32, f32, P, P, P], i32),
@@ -169,6 +171,23 @@ def tile_permute(x: torch.Tensor, lat, cfgs, out=None, meta=True):
     return out, cnt, mask
 
 
+def tile_permute_pool(x: torch.Tensor, lat, cfgs, out=None):
+    """Fused tiling + TripPool (one HBM pass): returns (x_tiled, tile_count, slot_mask, z)."""
+    _need_cuda(x)
+    assert x.dtype == torch.bfloat16 and x.dim() == 3 and x.stride(2) == 1
+    Hh, N, d = x.shape
+    sh = tiled_shape(lat, cfgs, Hh)
+    if out is None:
+        out = torch.empty((Hh, sh.n_tiles, sh.B, d), dtype=torch.bfloat16, device=x.device)
+    cnt = torch.empty((Hh, sh.n_tiles), dtype=torch.int32, device=x.device)
+    mask = torch.empty((Hh, sh.n_tiles, sh.B // 32), dtype=torch.int32, device=x.device)
+    z = torch.empty((Hh, sh.n_tiles, 3 * d), dtype=torch.float32, device=x.device)
+    st = load().veda_tile_permute_pool(_ptr(x), x.stride(0), x.stride(1), Latent(*lat), _cfg_array(cfgs, Hh), Hh, d,
+                                       _ptr(out), _ptr(cnt), _ptr(mask), _ptr(z), _stream())
+    _check(st, "tile_permute_pool")
+    return out, cnt, mask, z
+
+
 def tile_unpermute(o_tiled: torch.Tensor, lat, cfgs, out=None):
     """o_tiled [Hh,N_T,B,d] -> out [Hh, N, d] (or into a given [Hh,N,d] view)."""
     _need_cuda(o_tiled)
@@ -248,6 +267,20 @@ def tile_score(q_tiled, k_tiled, tile_count, slot_mask, scorer: Scorer, workspac
     return out
 
 
+def tile_score_pooled(zq, zk, tile_count, scorer: Scorer, workspace: ScoreWorkspace = None, out=None):
+    _need_cuda(zq, zk, tile_count)
+    Hh, NT, din = zq.shape
+    d = din // 3
+    if workspace is None:
+        workspace = ScoreWorkspace(Hh, NT, d, scorer, zq.device)
+    if out is None:
+        out = torch.empty((Hh, NT, NT), dtype=torch.float32, device=zq.device)
+    st = load().veda_tile_score_pooled(_ptr(zq), _ptr(zk), _ptr(tile_count), Hh, NT, d, ctypes.byref(scorer),
+                                       _ptr(out), _ptr(workspace.buf), workspace.nbytes, _stream())
+    _check(st, "tile_score_pooled")
+    return out
+
+
 def select_topk(scores: torch.Tensor, k: int, out=None):
     _need_cuda(scores)
     Hh, NT, _ = scores.shape
@@ -304,6 +337,8 @@ class SparseAttention:
         ev = events or [None] * 6
         if ev[0] is not None:
             ev[0].record()
+        # Q/K tiling and TripPool as two HBM-bound passes: measured faster than the fused
+        # veda_tile_permute_pool (its extra registers halve the occupancy of the copy)
         _check(lib.veda_tile_permute(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, _ptr(self.qt),
                                      _ptr(self.cnt), _ptr(self.mask), s), "tile_permute(q)")
         _check(lib.veda_tile_permute(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, _ptr(self.kt), None, None,

@@ -257,6 +257,23 @@ def test_zero_weights_select_first_valid_tiles(V):
         assert torch.equal(idx[h], valid.to(torch.int32).expand(idx.shape[1], 5))
 
 
+@pytest.mark.parametrize("name", ["tiny", "toy_b64_d128", "b128_d64", "mixed_cfgs"])
+def test_fused_permute_pool_and_pooled_score(V, name):
+    """veda_tile_permute_pool / veda_tile_score_pooled equal the unfused calls bit for bit."""
+    c = Case(name, **CASES[name])
+    dev = torch.device("cuda")
+    w = {n: t.to(dev) for n, t in c.w.items()}
+    q, k = c.q.to(dev), c.k.to(dev)
+    qt, cnt, mask = V.tile_permute(q, c.lat, c.cfgs)
+    kt, _, _ = V.tile_permute(k, c.lat, c.cfgs, meta=False)
+    qt2, cnt2, mask2, zq = V.tile_permute_pool(q, c.lat, c.cfgs)
+    kt2, _, _, zk = V.tile_permute_pool(k, c.lat, c.cfgs)
+    assert torch.equal(qt, qt2) and torch.equal(kt, kt2) and torch.equal(cnt, cnt2) and torch.equal(mask, mask2)
+    assert torch.equal(zq, V.trippool(qt, mask)) and torch.equal(zk, V.trippool(kt, mask))
+    sc = V.make_scorer(w)
+    assert torch.equal(V.tile_score_pooled(zq, zk, cnt, sc), V.tile_score(qt, kt, cnt, mask, sc))
+
+
 def test_nhd_layout_strided_permute(V):
     c = Case("toy_b128", **CASES["toy_b128"])
     dev = torch.device("cuda")
