@@ -306,6 +306,33 @@ def run_ours(args):
                "d2h_bytes_per_step": bo * world}
         del qh, kh, vh, oh, qd, kd, vd
 
+    # optional Ulysses mode (N > 1): sequence-sharded inputs [N_r, Hh, d], all-to-all to
+    # heads, local path, all-to-all back; its two exchanges are the only collectives
+    ulysses_ms = None
+    if world > 1:
+        from paper_2605_30325_b200 import ulysses as uly
+
+        del q, k, v, out
+        torch.cuda.empty_cache()
+        counts = uly.token_counts(pre.lat, world)
+        t0 = sum(counts[:rank])
+        fq, fk, fv = synth.qkv(pre, device=dev, layout="nhd")  # [N, Hh, d], all heads
+        ql, kl, vl = (t[t0:t0 + counts[rank]].contiguous() for t in (fq, fk, fv))
+        del fq, fk, fv
+        torch.cuda.empty_cache()
+        upath = uly.UlyssesSparseAttention(pre.lat, [pre.cfg], pre.heads, d, w, sparsity=sp, device=dev)
+        for _ in range(args.warmup):
+            upath(ql, kl, vl)
+        barrier()
+        u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        u0.record(stream)
+        for _ in range(args.steps):
+            upath(ql, kl, vl)
+        u1.record(stream)
+        barrier()
+        ulysses_ms = shard.max_over_ranks(u0.elapsed_time(u1) / args.steps)
+        del upath, ql, kl, vl
+
     peaks = load_peaks()
     flops = 4.0 * B * B * d * kk * NT * Hh  # executed QK^T + PV FLOPs per launch (this rank)
     achieved = flops / (parts["attn"] * 1e-3) / 1e12
@@ -346,6 +373,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "ulysses_ms_per_call": None if ulysses_ms is None else round(ulysses_ms, 3),
             "clocks": clock,
         }
         print(json.dumps(result), flush=True)

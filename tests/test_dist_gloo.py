@@ -95,3 +95,65 @@ def test_gloo_world2_sharded_equals_single(tmp_path):
     for h in range(len(CFGS)):
         assert np.array_equal(np.load(tmp_path / f"idx{h}.npy"), single["idx"][h])
         assert np.array_equal(np.load(tmp_path / f"o{h}.npy"), single["o"][h], equal_nan=True)
+
+
+# --------------------------------------------------------------------------- Ulysses exchange
+
+ULAT, UHH, UD = (5, 4, 6), 3, 8
+
+
+def _global_tensor(seed):
+    g = torch.Generator().manual_seed(seed)
+    return (torch.randn((ULAT[0] * ULAT[1] * ULAT[2], UHH, UD), generator=g) * 3).to(torch.bfloat16)
+
+
+def _ulysses_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_30325_b200 import ulysses
+    from paper_2605_30325_b200.shard import head_range
+
+    x = _global_tensor(1)
+    counts = ulysses.token_counts(ULAT, world)
+    start = sum(counts[:rank])
+    x_local = x[start:start + counts[rank]].contiguous()
+    xh = ulysses.seq_to_head(x_local, ULAT)
+    hr = head_range(UHH, rank, world)
+    ok1 = torch.equal(xh.view(torch.int16), x[:, hr.start:hr.stop, :].contiguous().view(torch.int16))
+    back = ulysses.head_to_seq(xh, ULAT, UHH)
+    ok2 = torch.equal(back.view(torch.int16), x_local.view(torch.int16))
+    # full path on the head shard with the oracle as the kernel backend, then back to sequence
+    res = _path_on_heads(xh, hr)
+    o_seq = ulysses.head_to_seq(res, ULAT, UHH)
+    np.save(os.path.join(out_dir, f"o{rank}.npy"), o_seq.view(torch.int16).numpy())
+    np.save(os.path.join(out_dir, f"ok{rank}.npy"), np.array([ok1, ok2]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _path_on_heads(x_heads, hr):
+    """Oracle attention (dense over tiles, k = N_T) of [N, Hh_r, d] with q = k = v = x."""
+    import oracle
+
+    oracle.build()
+    cfg = [(1, 2, 2)] * len(hr)
+    xb = x_heads.transpose(0, 1).contiguous().view(torch.int16).numpy().view(np.uint16)
+    xt, cnt, mask = oracle.tile_permute(xb, ULAT, cfg)
+    NT = xt.shape[1]
+    idx = np.broadcast_to(np.arange(NT, dtype=np.int32), (len(hr), NT, NT)).copy()
+    o = oracle.sparse_attn(xt, xt, xt, idx, mask, nthreads=1)
+    ob = oracle.tile_unpermute(oracle.f64_to_bf16_bits(o), ULAT, cfg)  # [Hh_r, N, d]
+    return torch.from_numpy(ob.view(np.int16)).view(torch.bfloat16).transpose(0, 1).contiguous()
+
+
+def test_ulysses_exchange_world2(tmp_path):
+    world, port = 2, _free_port()
+    mp.spawn(_ulysses_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    x = _global_tensor(1)
+    full = _path_on_heads(x, range(UHH))  # single process, all heads
+    counts = [len(range((r * ULAT[0]) // world, ((r + 1) * ULAT[0]) // world)) * ULAT[1] * ULAT[2] for r in range(world)]
+    for r in range(world):
+        assert np.load(tmp_path / f"ok{r}.npy").all()
+        start = sum(counts[:r])
+        want = full[start:start + counts[r]].view(torch.int16).numpy()
+        assert np.array_equal(np.load(tmp_path / f"o{r}.npy"), want)
