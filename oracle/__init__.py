@@ -57,6 +57,10 @@ def _load():
         lib.vo_scores.restype = None
         lib.vo_topk.argtypes = [P, i64, i64, i32, P]
         lib.vo_sparse_attn.argtypes = [P, P, P, P, P, i32, i64, i32, i32, i32, dbl, P, i64, P, P, i32]
+        lib.vo_target_scores.argtypes = [P, P, P, i32, i64, i32, i32, dbl, P, i64, P, i32]
+        lib.vo_target_scores.restype = None
+        lib.vo_recall.argtypes = [P, P, P, i64, i32]
+        lib.vo_recall.restype = dbl
         _lib = lib
     return _lib
 
@@ -198,6 +202,35 @@ def sparse_attn(qt, kt, vt, idx, mask, scale: float = 0.0, units=None, nthreads:
     if rc:
         raise ValueError("k out of range")
     return (o, lse) if want_lse else o
+
+
+def target_scores(qt, kt, mask, scale: float = 0.0, units=None, nthreads: int | None = None):
+    """Eq. 4: S_tgt_ij = max over the (i, j) tile block of A* = softmax(Q K^T / sqrt(d)).
+    Returns [Hh, N_T, N_T] fp64 (rows of units not listed are NaN)."""
+    qt = np.ascontiguousarray(qt, dtype=np.uint16)
+    kt = np.ascontiguousarray(kt, dtype=np.uint16)
+    mask = np.ascontiguousarray(mask, dtype=np.uint32)
+    Hh, NT, B, d = qt.shape
+    s = np.full((Hh, NT, NT), np.nan, dtype=np.float64)
+    if units is not None:
+        u = np.ascontiguousarray(np.asarray(list(units), dtype=np.int64))
+        up, nu = _p(u), len(u)
+    else:
+        up, nu = None, 0
+    if nthreads is None:
+        nthreads = len(os.sched_getaffinity(0))
+    _load().vo_target_scores(_p(qt), _p(kt), _p(mask), Hh, NT, B, d, float(scale), up, nu, _p(s), int(nthreads))
+    return s
+
+
+def recall(idx_sp, idx_fu, cnt=None) -> float:
+    """Eq. 3: mean over (real) query tiles of |S_sp & S_fu| / k."""
+    a = np.ascontiguousarray(idx_sp, dtype=np.int32)
+    b = np.ascontiguousarray(idx_fu, dtype=np.int32)
+    k = a.shape[-1]
+    rows = int(np.prod(a.shape[:-1]))
+    c = np.ascontiguousarray(cnt, dtype=np.int32) if cnt is not None else None
+    return float(_load().vo_recall(_p(a), _p(b), _p(c) if c is not None else None, rows, k))
 
 
 def bf16_bits_to_f64(x: np.ndarray) -> np.ndarray:

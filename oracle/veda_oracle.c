@@ -388,3 +388,120 @@ int vo_sparse_attn(const uint16_t *qt, const uint16_t *kt, const uint16_t *vt,
     pthread_mutex_destroy(&J.mu);
     return 0;
 }
+
+/* ------------------------------------------------------------------------- *
+ * NEXT-2a  Target tile scores, Eq. 4: PAPER.md:253-258 (section 4.1)
+ *     A* = Softmax(Q K^T / sqrt(d)),   S_tgt_ij = max_{(u,v) in Tile(i,j)} A*_uv
+ * (Alg. 3 "MaxPool(A*, kernel=B, stride=B)").  Reading R4: the softmax runs
+ * over the real keys of the whole sequence; padded query slots are dropped from the
+ * max; a key tile without real tokens scores -inf (as in S_pred, R5); a query tile
+ * without real tokens gets a row of 0 (its outputs are discarded anyway).
+ *   qt, kt [Hh][N_T][B][d] bf16 bits; mask [Hh][N_T][MW]; s [Hh][N_T][N_T] fp64
+ *   units: optional list of query tiles u = h*N_T + i to compute (NULL = all)
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    const uint16_t *qt, *kt;
+    const uint32_t *mask;
+    int64_t NT;
+    int B, d;
+    double scale;
+    const int64_t *units;
+    int64_t n_units;
+    double *s;
+    int64_t next;
+    pthread_mutex_t mu;
+} tgt_job;
+
+static void tgt_unit(tgt_job *J, int64_t u, double *logit)
+{
+    const int B = J->B, d = J->d;
+    const int64_t NT = J->NT, MW = (B + 31) / 32, h = u / NT;
+    double *row = J->s + u * NT;
+    for (int64_t j = 0; j < NT; ++j) {
+        int any = 0;
+        for (int b = 0; b < B; ++b) any |= slot_valid(J->mask + (h * NT + j) * MW, b);
+        row[j] = any ? 0.0 : -INFINITY;
+    }
+    const uint32_t *mq = J->mask + u * MW;
+    for (int a = 0; a < B; ++a) {
+        if (!slot_valid(mq, a)) continue;
+        const uint16_t *q = J->qt + (u * B + a) * d;
+        /* full softmax over every real key of head h */
+        double mx = -INFINITY;
+        for (int64_t j = 0; j < NT; ++j)
+            for (int b = 0; b < B; ++b) {
+                double *l = logit + j * B + b;
+                if (!slot_valid(J->mask + (h * NT + j) * MW, b)) { *l = -INFINITY; continue; }
+                const uint16_t *kk = J->kt + ((h * NT + j) * B + b) * d;
+                double acc = 0.0;
+                for (int c = 0; c < d; ++c) acc += bf16_to_f64(q[c]) * bf16_to_f64(kk[c]);
+                *l = acc * J->scale;
+                if (*l > mx) mx = *l;
+            }
+        double z = 0.0;
+        for (int64_t r = 0; r < NT * B; ++r)
+            if (logit[r] != -INFINITY) z += exp(logit[r] - mx);
+        /* max-pool of A*_uv over each key tile */
+        for (int64_t j = 0; j < NT; ++j)
+            for (int b = 0; b < B; ++b) {
+                const double l = logit[j * B + b];
+                if (l == -INFINITY) continue;
+                const double p = exp(l - mx) / z;
+                if (p > row[j]) row[j] = p;
+            }
+    }
+}
+
+static void *tgt_worker(void *arg)
+{
+    tgt_job *J = (tgt_job *)arg;
+    double *logit = (double *)malloc(sizeof(double) * (size_t)(J->NT * J->B));
+    for (;;) {
+        pthread_mutex_lock(&J->mu);
+        const int64_t w = J->next++;
+        pthread_mutex_unlock(&J->mu);
+        if (w >= J->n_units) break;
+        tgt_unit(J, J->units ? J->units[w] : w, logit);
+    }
+    free(logit);
+    return NULL;
+}
+
+void vo_target_scores(const uint16_t *qt, const uint16_t *kt, const uint32_t *mask, int Hh, int64_t NT, int B,
+                      int d, double scale, const int64_t *units, int64_t n_units, double *s, int nthreads)
+{
+    tgt_job J;
+    J.qt = qt; J.kt = kt; J.mask = mask; J.NT = NT; J.B = B; J.d = d;
+    J.scale = scale > 0 ? scale : 1.0 / sqrt((double)d);
+    J.units = units; J.n_units = units ? n_units : (int64_t)Hh * NT; J.s = s; J.next = 0;
+    pthread_mutex_init(&J.mu, NULL);
+    if (nthreads < 1) nthreads = 1;
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, tgt_worker, &J);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    free(th);
+    pthread_mutex_destroy(&J.mu);
+}
+
+/* ------------------------------------------------------------------------- *
+ * NEXT-2b  Tile recall, Eq. 3: PAPER.md:225-233 (section 3.2)
+ *     Recall@k = (1 / N_T) sum_i |S_i^sp intersect S_i^fu| / k
+ * with S^sp the predicted kept set and S^fu the oracle (full-attention) set of query
+ * tile i.  Reading R4: the mean runs over query tiles that hold at least one real token
+ * (cnt > 0).  Returns the recall; idx lists [rows][k] (any order).
+ * ------------------------------------------------------------------------- */
+double vo_recall(const int32_t *idx_sp, const int32_t *idx_fu, const int32_t *cnt, int64_t rows, int k)
+{
+    double acc = 0.0;
+    int64_t n = 0;
+    for (int64_t r = 0; r < rows; ++r) {
+        if (cnt && cnt[r] == 0) continue;
+        int inter = 0;
+        for (int a = 0; a < k; ++a)
+            for (int b = 0; b < k; ++b)
+                if (idx_sp[r * k + a] == idx_fu[r * k + b]) { ++inter; break; }
+        acc += (double)inter / (double)k;
+        ++n;
+    }
+    return n ? acc / (double)n : 0.0;
+}
