@@ -190,6 +190,32 @@ VEDA_API veda_status veda_pair_scores(const double *eq, const double *ek, const 
                              int32_t Hh, int32_t n_tiles, int32_t d_lat, float *scores,
                              void *stream);
 
+/* ---- oracle tile mask and recall -------------------------- */
+
+/* Exact pooled target scores, Eq. 4 (Alg. 3):
+ *   S_tgt[h][i][j] = max over real (u in tile i, v in tile j) of A*_uv,
+ *   A* = softmax(Q K^T * scale) over ALL real keys of head h,
+ * computed as exp(max_u(max_v s_uv * scale - lse_u)) -- the second of the two passes of
+ * PAPER.md:412-416.  lse [Hh][N_T][B] fp32 (natural log) is pass 1: the lse output of
+ * veda_sparse_attn_fwd run densely (k = N_T, idx[i] = 0..N_T-1) on the same q/k.
+ * Empty key tile -> -inf; query tile without real tokens -> 0 (readings R4, R5, R19).
+ * bf16 operands, fp32 accumulation (tcgen05 / TMEM); softmax_scale <= 0 -> 1/sqrt(d).
+ *   s_tgt : [Hh][N_T][N_T] fp32 (device).  B in {64, 128}, d in {64, 128}.
+ * Feeding s_tgt to veda_select_topk gives the oracle mask M~* (Eq. 4).      */
+VEDA_API veda_status veda_target_scores(const uint16_t *q_tiled, const uint16_t *k_tiled,
+                               const uint32_t *slot_mask, const float *lse, int32_t Hh,
+                               int32_t n_tiles, int32_t B, int32_t d, float softmax_scale,
+                               float *s_tgt, void *stream);
+
+/* Tile recall, Eq. 3: Recall@k = mean over query tiles i of
+ * |S_sp,i intersect S_fu,i| / k, over the rows whose tile_count > 0 (R4; tile_count
+ * may be NULL = all rows).  idx_sp / idx_fu : [rows][k] int32 key-tile lists (any order,
+ * no duplicates; entries outside [0, n_tiles) never match).  recall : one fp64 on the
+ * DEVICE (0 when no row counts).  Integer counts, one fp64 division: deterministic.  */
+VEDA_API veda_status veda_tile_recall(const int32_t *idx_sp, const int32_t *idx_fu,
+                             const int32_t *tile_count, int64_t rows, int32_t n_tiles,
+                             int32_t k, double *recall, void *stream);
+
 /* ---- diagnostics ------------------------------------------------------------------ */
 VEDA_API const char *veda_status_str(veda_status st);
 VEDA_API const char *veda_last_error(void);

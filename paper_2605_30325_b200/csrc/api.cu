@@ -356,6 +356,32 @@ veda_status veda_sparse_attn_fwd(const uint16_t *q_tiled, const uint16_t *k_tile
                               S(stream));
 }
 
+veda_status veda_target_scores(const uint16_t *q_tiled, const uint16_t *k_tiled, const uint32_t *slot_mask,
+                               const float *lse, int32_t Hh, int32_t n_tiles, int32_t B, int32_t d,
+                               float softmax_scale, float *s_tgt, void *stream)
+{
+    if (!q_tiled || !k_tiled || !slot_mask || !lse || !s_tgt) return fail(VEDA_ERR_NULL, "target_scores: NULL pointer");
+    if (Hh < 1 || n_tiles < 1 || (int64_t)Hh * n_tiles * B > INT32_MAX)
+        return fail(VEDA_ERR_SHAPE, "target_scores: bad sizes");
+    if (!aligned16(q_tiled) || !aligned16(k_tiled))
+        return fail(VEDA_ERR_ALIGN, "target_scores: tensors must be 16-byte aligned");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)d);
+    return launch_target_scores(q_tiled, k_tiled, slot_mask, lse, Hh, n_tiles, B, d, scale, s_tgt, S(stream));
+}
+
+veda_status veda_tile_recall(const int32_t *idx_sp, const int32_t *idx_fu, const int32_t *tile_count, int64_t rows,
+                             int32_t n_tiles, int32_t k, double *recall, void *stream)
+{
+    if (!idx_sp || !idx_fu || !recall) return fail(VEDA_ERR_NULL, "tile_recall: NULL pointer");
+    if (rows < 1 || n_tiles < 1) return fail(VEDA_ERR_SHAPE, "tile_recall: bad sizes");
+    if (k < 1 || k > n_tiles) return fail(VEDA_ERR_K_RANGE, "tile_recall: k=%d outside [1, %d]", k, n_tiles);
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    return launch_recall(idx_sp, idx_fu, tile_count, rows, n_tiles, k, recall, S(stream));
+}
+
 const char *veda_status_str(veda_status st)
 {
     switch (st) {

@@ -27,7 +27,8 @@ VEDA_STATUS = ["VEDA_OK", "VEDA_ERR_NULL", "VEDA_ERR_SHAPE", "VEDA_ERR_CONFIG", 
 EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_workspace", "veda_tile_permute",
            "veda_tile_score", "veda_select_topk", "veda_sparse_attn_fwd", "veda_tile_unpermute",
            "veda_trippool", "veda_project", "veda_pair_scores", "veda_status_str", "veda_last_error",
-           "veda_launch_count", "veda_check_device", "veda_tile_permute_pool", "veda_tile_score_pooled"]
+           "veda_launch_count", "veda_check_device", "veda_tile_permute_pool", "veda_tile_score_pooled",
+           "veda_target_scores", "veda_tile_recall"]
 
 
 class VedaError(RuntimeError):
@@ -79,6 +80,8 @@ def load(path: str = LIB_PATH):
         "veda_trippool": ([P, P, i32, i32, i32, i32, P, P], i32),
         "veda_project": ([P, i32, i32, i32, i32, i32, P, P, P, P, P, P, P], i32),
         "veda_pair_scores": ([P, P, P, i32, i32, i32, P, P], i32),
+        "veda_target_scores": ([P, P, P, P, i32, i32, i32, i32, f32, P, P], i32),
+        "veda_tile_recall": ([P, P, P, i64, i32, i32, P, P], i32),
         "veda_status_str": ([i32], ctypes.c_char_p),
         "veda_last_error": ([], ctypes.c_char_p),
         "veda_launch_count": ([], ctypes.c_uint64),
@@ -301,6 +304,43 @@ def sparse_attn_fwd(q_tiled, k_tiled, v_tiled, idx, slot_mask, scale: float = 0.
                                      NT, B, d, k, float(scale), _ptr(out), _ptr(lse), _stream())
     _check(st, "sparse_attn_fwd")
     return (out, lse) if want_lse else out
+
+
+def target_scores(q_tiled, k_tiled, slot_mask, lse, scale: float = 0.0, out=None):
+    """Eq. 4 pass 2: S_tgt [Hh, N_T, N_T] fp32 from the dense lse (see oracle_tile_mask)."""
+    _need_cuda(q_tiled, k_tiled, slot_mask, lse)
+    Hh, NT, B, d = q_tiled.shape
+    if out is None:
+        out = torch.empty((Hh, NT, NT), dtype=torch.float32, device=q_tiled.device)
+    st = load().veda_target_scores(_ptr(q_tiled), _ptr(k_tiled), _ptr(slot_mask), _ptr(lse), Hh, NT, B, d,
+                                   float(scale), _ptr(out), _stream())
+    _check(st, "target_scores")
+    return out
+
+
+def oracle_tile_mask(q_tiled, k_tiled, v_tiled, slot_mask, k: int, scale: float = 0.0):
+    """The oracle mask M~* of Eq. 4 / Alg. 3, both passes on the GPU:
+    pass 1 = dense veda_sparse_attn_fwd (k = N_T) for the row lse, pass 2 =
+    veda_target_scores, then veda_select_topk.  Returns (idx [Hh,N_T,k], S_tgt)."""
+    Hh, NT, B, d = q_tiled.shape
+    dense = torch.arange(NT, dtype=torch.int32, device=q_tiled.device).expand(Hh, NT, NT).contiguous()
+    _, lse = sparse_attn_fwd(q_tiled, k_tiled, v_tiled, dense, slot_mask, scale=scale, want_lse=True)
+    s_tgt = target_scores(q_tiled, k_tiled, slot_mask, lse, scale=scale)
+    return select_topk(s_tgt, k), s_tgt
+
+
+def tile_recall(idx_sp, idx_fu, tile_count=None, n_tiles=None, out=None):
+    """Eq. 3 Recall@k (device fp64 scalar tensor).  idx [..., k]; n_tiles defaults to
+    idx_sp.shape[-2] (square [Hh, N_T, k] lists)."""
+    _need_cuda(idx_sp, idx_fu)
+    k = idx_sp.shape[-1]
+    NT = int(n_tiles) if n_tiles is not None else idx_sp.shape[-2]
+    rows = idx_sp.numel() // k
+    if out is None:
+        out = torch.empty((), dtype=torch.float64, device=idx_sp.device)
+    st = load().veda_tile_recall(_ptr(idx_sp), _ptr(idx_fu), _ptr(tile_count), rows, NT, k, _ptr(out), _stream())
+    _check(st, "tile_recall")
+    return out
 
 
 class SparseAttention:
