@@ -251,7 +251,9 @@ def run_ours(args):
     def dense():
         veda.sparse_attn_fwd(path.qt, path.kt, path.vt, idx_dense, path.mask, out=dense_out)
 
-    dense()
+    # warm-up dense call doubles as pass 1 of the oracle tile mask (Eq. 4): row lse
+    _, lse_dense = veda.sparse_attn_fwd(path.qt, path.kt, path.vt, idx_dense, path.mask, out=dense_out,
+                                        want_lse=True)
     barrier()
     d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     d0.record(stream)
@@ -261,6 +263,17 @@ def run_ours(args):
     barrier()
     dense_ms = shard.max_over_ranks(d0.elapsed_time(d1) / args.dense_steps)
     del idx_dense, dense_out
+
+    # recall (Eq. 3) of the path's kept lists against the oracle mask M~* = TopK(S_tgt),
+    # S_tgt from veda_target_scores (Eq. 4 pass 2); untimed, quality context only
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    s_tgt = veda.target_scores(path.qt, path.kt, path.mask, lse_dense)
+    t1.record(stream)
+    idx_star = veda.select_topk(s_tgt, kk)
+    recall = veda.tile_recall(path.idx, idx_star, path.cnt).item()
+    target_ms = shard.max_over_ranks(t0.elapsed_time(t1))
+    del s_tgt, idx_star, lse_dense
 
     # attention kernel with uniformly random lists (regime R2, L2 worst case)
     ridx = synth.random_index_lists(Hh, NT, kk, seed_parts=("R2", args.workload, heads.start)).to(dev)
@@ -366,6 +379,9 @@ def run_ours(args):
             "attn_kernel_ms": round(attn_ms, 3),
             "attn_kernel_ms_random_lists": round(rand_attn_ms, 3),
             "step_breakdown_ms": {n: round(t, 3) for n, t in parts.items()},
+            "recall_vs_oracle_mask": {"value": round(recall, 4), "chance": round(kk / NT, 4),
+                                      "scorer": "random-init (no distilled weights)",
+                                      "target_kernel_ms": round(target_ms, 2)},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1),
                          "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
                          "frac": round(achieved / peaks["bf16_tflops_sustained"], 3), "traffic": traffic,
