@@ -233,6 +233,81 @@ def recall(idx_sp, idx_fu, cnt=None) -> float:
     return float(_load().vo_recall(_p(a), _p(b), _p(c) if c is not None else None, rows, k))
 
 
+def omega(B: int):
+    """Eq. 8 search space (Alg. 1 l.640): all (p_t, p_h, p_w) in N^3 with
+    p_t p_h p_w = B, in lexicographic order."""
+    out = []
+    for pt in range(1, B + 1):
+        if B % pt:
+            continue
+        for ph in range(1, B // pt + 1):
+            if (B // pt) % ph:
+                continue
+            out.append((pt, ph, B // (pt * ph)))
+    return out
+
+
+def token_index(lat, cfgs, Hh: int):
+    """perm [Hh, N_T*B]: token index held by each tiled slot (-1 for padding), obtained by
+    tiling a payload of token ids with vo_tile_permute."""
+    N = lat[0] * lat[1] * lat[2]
+    n = np.arange(N, dtype=np.int64)
+    x = np.zeros((Hh, N, 2), dtype=np.uint16)
+    x[:, :, 0] = (n & 0xFFFF).astype(np.uint16)
+    x[:, :, 1] = (n >> 16).astype(np.uint16)
+    xt, cnt, mask = tile_permute(x, lat, cfgs)
+    Hh_, NT, B, _ = xt.shape
+    tok = xt[..., 0].astype(np.int64) | (xt[..., 1].astype(np.int64) << 16)
+    bits = ((mask[..., :, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(Hh_, NT, -1)[..., :B]
+    return np.where(bits.astype(bool), tok, -1).reshape(Hh_, NT * B)
+
+
+def full_attention(q, k, v, scale: float = 0.0):
+    """Alg. 1 l.647-648: A_fu = softmax(Q K^T / sqrt(d)), O_fu = A_fu V per head on the
+    untiled tokens (numpy fp64 matmul as the library step).  Returns O_fu [Hh, N, d]."""
+    qd, kd, vd = (bf16_bits_to_f64(a) for a in (q, k, v))
+    d = qd.shape[-1]
+    sc = scale if scale > 0 else 1.0 / np.sqrt(d)
+    out = np.empty_like(qd)
+    for h in range(qd.shape[0]):
+        l = (qd[h] @ kd[h].T) * sc
+        l -= l.max(axis=1, keepdims=True)
+        a = np.exp(l)
+        a /= a.sum(axis=1, keepdims=True)
+        out[h] = a @ vd[h]
+    return out
+
+
+def tiling_search_errors(q, k, v, lat, k_top: int, cands=None, o_fu=None, nthreads=None):
+    """Alg. 1, Eq. 9, one calibration sample:
+    for every candidate pi: tile Q, K, V with pi (l.652); oracle mask M~ = Top-k of the
+    max-pooled full attention map (l.653-656; RowNorm is a positive per-row scale and does
+    not change a row's Top-k, reading R20); O_sp = UnTile(SparseAttn(Q~, K~, V~, M~)) (l.658);
+    E[h, pi] = ||O_fu - O_sp||_F^2 over the real tokens (l.659).
+    k_top is clamped to N_T(pi) (R20).  Returns E [Hh, |cands|] fp64."""
+    q = np.ascontiguousarray(q, dtype=np.uint16)
+    Hh, N, d = q.shape
+    cands = list(cands) if cands is not None else omega(128)
+    if o_fu is None:
+        o_fu = full_attention(q, k, v)
+    E = np.zeros((Hh, len(cands)))
+    for c, pi in enumerate(cands):
+        qt, cnt, mask = tile_permute(q, lat, [pi])
+        kt, _, _ = tile_permute(k, lat, [pi])
+        vt, _, _ = tile_permute(v, lat, [pi])
+        NT = qt.shape[1]
+        s = target_scores(qt, kt, mask, nthreads=nthreads)
+        idx = topk(s, min(k_top, NT))
+        o_t = sparse_attn(qt, kt, vt, idx, mask, nthreads=nthreads)
+        perm = token_index(lat, [pi], Hh)
+        for h in range(Hh):
+            real = perm[h] >= 0
+            o_sp = np.empty((N, d))
+            o_sp[perm[h][real]] = o_t[h].reshape(-1, d)[real]
+            E[h, c] = ((o_fu[h] - o_sp) ** 2).sum()
+    return E
+
+
 def bf16_bits_to_f64(x: np.ndarray) -> np.ndarray:
     """Exact widening of bf16 bit patterns (for pins written in numpy)."""
     return (np.asarray(x, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
