@@ -216,6 +216,30 @@ VEDA_API veda_status veda_tile_recall(const int32_t *idx_sp, const int32_t *idx_
                              const int32_t *tile_count, int64_t rows, int32_t n_tiles,
                              int32_t k, double *recall, void *stream);
 
+/* ---- head-aware tiling search support (Alg. 1, Eq. 8-9) -------- */
+
+/* Per-token fp32 values -> tiled layout of `cfg` (same boxes/slots as veda_tile_permute):
+ * x_tiled[h][i][b] = x[h*head_stride + n(h,i,b)], `pad` for padded slots.  Used to carry
+ * the full-attention row lse (a property of the token, not of the tiling, PAPER.md:
+ * 647-648) into each candidate tiling of Alg. 1, so one dense pass serves all of Omega.
+ *   x : [Hh][N] (head_stride >= N), x_tiled : [Hh][N_T][B]                              */
+VEDA_API veda_status veda_tile_permute_scalar(const float *x, int64_t head_stride, veda_latent lat,
+                                     const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh,
+                                     float pad, float *x_tiled, void *stream);
+
+/* Inverse on real slots: x[h*head_stride + n] = x_tiled[h][i][b]; padded slots dropped. */
+VEDA_API veda_status veda_tile_unpermute_scalar(const float *x_tiled, veda_latent lat,
+                                       const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh,
+                                       float *x, int64_t head_stride, void *stream);
+
+/* Alg. 1: err[h] += sum_e (a[h][e] - b[h][e])^2 over n bf16 elements per head
+ * (a, b at a + h*head_stride; n and head_stride multiples of 8).  Differences and squares
+ * are exact in fp64; partial sums fp64 (per-CTA partials combined with fp64 atomics, so
+ * run-to-run differences are at the 1e-16 relative level).  err : [Hh] fp64, device,
+ * ACCUMULATED (zero it to start a calibration set).                                    */
+VEDA_API veda_status veda_sq_err(const uint16_t *a, const uint16_t *b, int64_t head_stride,
+                        int64_t n, int32_t Hh, double *err, void *stream);
+
 /* ---- diagnostics ------------------------------------------------------------------ */
 VEDA_API const char *veda_status_str(veda_status st);
 VEDA_API const char *veda_last_error(void);

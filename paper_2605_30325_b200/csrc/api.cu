@@ -382,6 +382,49 @@ veda_status veda_tile_recall(const int32_t *idx_sp, const int32_t *idx_fu, const
     return launch_recall(idx_sp, idx_fu, tile_count, rows, n_tiles, k, recall, S(stream));
 }
 
+veda_status veda_tile_permute_scalar(const float *x, int64_t head_stride, veda_latent lat, const veda_tile_cfg *cfg,
+                                     int32_t Hh, float pad, float *x_tiled, void *stream)
+{
+    if (!x || !x_tiled) return fail(VEDA_ERR_NULL, "tile_permute_scalar: NULL tensor");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    Shape sh;
+    HeadCfgs hc;
+    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    if (head_stride < (int64_t)lat.t * lat.h * lat.w)
+        return fail(VEDA_ERR_SHAPE, "tile_permute_scalar: head_stride < N");
+    return launch_permute_scalar(x, head_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B, sh.NT, pad,
+                                 x_tiled, S(stream));
+}
+
+veda_status veda_tile_unpermute_scalar(const float *x_tiled, veda_latent lat, const veda_tile_cfg *cfg, int32_t Hh,
+                                       float *x, int64_t head_stride, void *stream)
+{
+    if (!x || !x_tiled) return fail(VEDA_ERR_NULL, "tile_unpermute_scalar: NULL tensor");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    Shape sh;
+    HeadCfgs hc;
+    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    if (head_stride < (int64_t)lat.t * lat.h * lat.w)
+        return fail(VEDA_ERR_SHAPE, "tile_unpermute_scalar: head_stride < N");
+    return launch_unpermute_scalar(x_tiled, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B, sh.NT, x,
+                                   head_stride, S(stream));
+}
+
+veda_status veda_sq_err(const uint16_t *a, const uint16_t *b, int64_t head_stride, int64_t n, int32_t Hh,
+                        double *err, void *stream)
+{
+    if (!a || !b || !err) return fail(VEDA_ERR_NULL, "sq_err: NULL pointer");
+    if (Hh < 1 || n < 0 || Hh > 65535 || head_stride < n) return fail(VEDA_ERR_SHAPE, "sq_err: bad sizes");
+    if ((n % 8) || (head_stride % 8) || !aligned16(a) || !aligned16(b))
+        return fail(VEDA_ERR_ALIGN, "sq_err: n, head_stride must be multiples of 8, pointers 16-byte aligned");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    if (n == 0) return VEDA_OK;
+    return launch_sq_err(a, b, head_stride, n, Hh, err, S(stream));
+}
+
 const char *veda_status_str(veda_status st)
 {
     switch (st) {

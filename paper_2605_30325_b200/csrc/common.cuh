@@ -50,6 +50,12 @@ veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint1
                                int kk, float scale, uint16_t *o, float *lse, cudaStream_t s);
 veda_status launch_target_scores(const uint16_t *q, const uint16_t *k, const uint32_t *mask, const float *lse,
                                  int Hh, int NT, int B, int d, float scale, float *out, cudaStream_t s);
+veda_status launch_permute_scalar(const float *x, int64_t hs, const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp,
+                                  int T, int H, int W, int B, int NT, float pad, float *xt, cudaStream_t s);
+veda_status launch_unpermute_scalar(const float *xt, const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp, int T,
+                                    int H, int W, int B, int NT, float *x, int64_t hs, cudaStream_t s);
+veda_status launch_sq_err(const uint16_t *a, const uint16_t *b, int64_t hs, int64_t n, int Hh, double *err,
+                          cudaStream_t s);
 veda_status launch_recall(const int32_t *sp, const int32_t *fu, const int32_t *cnt, int64_t rows, int NT, int k,
                           double *recall, cudaStream_t s);
 

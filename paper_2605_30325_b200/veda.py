@@ -28,7 +28,8 @@ EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_worksp
            "veda_tile_score", "veda_select_topk", "veda_sparse_attn_fwd", "veda_tile_unpermute",
            "veda_trippool", "veda_project", "veda_pair_scores", "veda_status_str", "veda_last_error",
            "veda_launch_count", "veda_check_device", "veda_tile_permute_pool", "veda_tile_score_pooled",
-           "veda_target_scores", "veda_tile_recall"]
+           "veda_target_scores", "veda_tile_recall", "veda_tile_permute_scalar", "veda_tile_unpermute_scalar",
+           "veda_sq_err"]
 
 
 class VedaError(RuntimeError):
@@ -82,6 +83,9 @@ def load(path: str = LIB_PATH):
         "veda_pair_scores": ([P, P, P, i32, i32, i32, P, P], i32),
         "veda_target_scores": ([P, P, P, P, i32, i32, i32, i32, f32, P, P], i32),
         "veda_tile_recall": ([P, P, P, i64, i32, i32, P, P], i32),
+        "veda_tile_permute_scalar": ([P, i64, Latent, P, i32, f32, P, P], i32),
+        "veda_tile_unpermute_scalar": ([P, Latent, P, i32, P, i64, P], i32),
+        "veda_sq_err": ([P, P, i64, i64, i32, P, P], i32),
         "veda_status_str": ([i32], ctypes.c_char_p),
         "veda_last_error": ([], ctypes.c_char_p),
         "veda_launch_count": ([], ctypes.c_uint64),
@@ -203,6 +207,44 @@ def tile_unpermute(o_tiled: torch.Tensor, lat, cfgs, out=None):
                                     out.stride(0), out.stride(1), _stream())
     _check(st, "tile_unpermute")
     return out
+
+
+def tile_permute_scalar(x: torch.Tensor, lat, cfgs, pad: float = 0.0, out=None):
+    """Per-token fp32 x [Hh, N] (last stride 1) -> [Hh, N_T, B] in the tiling of cfgs."""
+    _need_cuda(x)
+    Hh = x.shape[0]
+    sh = tiled_shape(lat, cfgs, Hh)
+    if out is None:
+        out = torch.empty((Hh, sh.n_tiles, sh.B), dtype=torch.float32, device=x.device)
+    assert x.dtype == torch.float32 and x.stride(-1) == 1
+    st = load().veda_tile_permute_scalar(_ptr(x), x.stride(0), Latent(*lat), _cfg_array(cfgs, Hh), Hh, float(pad),
+                                         _ptr(out), _stream())
+    _check(st, "tile_permute_scalar")
+    return out
+
+
+def tile_unpermute_scalar(x_tiled: torch.Tensor, lat, cfgs, out=None):
+    """[Hh, N_T, B] fp32 -> per-token [Hh, N] (padded slots dropped)."""
+    _need_cuda(x_tiled)
+    Hh = x_tiled.shape[0]
+    N = lat[0] * lat[1] * lat[2]
+    if out is None:
+        out = torch.empty((Hh, N), dtype=torch.float32, device=x_tiled.device)
+    st = load().veda_tile_unpermute_scalar(_ptr(x_tiled), Latent(*lat), _cfg_array(cfgs, Hh), Hh, _ptr(out),
+                                           out.stride(0), _stream())
+    _check(st, "tile_unpermute_scalar")
+    return out
+
+
+def sq_err(a: torch.Tensor, b: torch.Tensor, err: torch.Tensor):
+    """err[h] += ||a[h] - b[h]||_F^2 for bf16 [Hh, ...] tensors (contiguous); err fp64 [Hh]."""
+    _need_cuda(a, b, err)
+    assert a.shape == b.shape and a.is_contiguous() and b.is_contiguous() and err.dtype == torch.float64
+    Hh = a.shape[0]
+    n = a[0].numel()
+    st = load().veda_sq_err(_ptr(a), _ptr(b), n, n, Hh, _ptr(err), _stream())
+    _check(st, "sq_err")
+    return err
 
 
 def trippool(x_tiled: torch.Tensor, slot_mask: torch.Tensor):
