@@ -24,6 +24,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -294,7 +295,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // stage) are probed in ONE asm block so their latencies overlap; only a barrier
         // that is not yet complete is then waited on.  Ring stages are released by the
         // softmax warps; the MMA thread only commits S_FULL (+ Q_EMPTY / O_FULL).
-        if (lane == 0) {
+        // The whole warp runs the loop (warp-uniform values, one lane issues via elect.sync:
+        // see sm100.cuh mma_ss_w); descriptors are advanced by constant offsets.
+        {
             constexpr uint32_t idesc_qk = idesc_bf16_f32(128, B, 0, 0);  // Q, K both K-major
             constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D, 0, 1);  // P K-major (TMEM), V MN-major
             uint32_t stage = 0, ph = 0;
@@ -307,28 +310,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (++stage == G::NST) { stage = 0; ph ^= 1; }
             };
             auto issue_qk = [&](int s, int t, uint32_t st) {
-                const uint32_t qa = sQ + s * G::Q_BYTES, kb = sRing + st * G::TILE_BYTES;
+                const uint64_t ad0 = sdesc_sw128(sQ + s * G::Q_BYTES, 16, 1024);
+                const uint64_t bd0 = sdesc_sw128(sRing + st * G::TILE_BYTES, 16, 1024);
                 const uint32_t tS = tbase + s * 256;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint64_t ad = sdesc_sw128(qa + (kk >> 2) * G::QCHUNK + (kk & 3) * 32, 16, 1024);
-                    const uint64_t bd = sdesc_sw128(kb + (kk >> 2) * G::KCHUNK + (kk & 3) * 32, 16, 1024);
-                    mma_ss(tS, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+                    const uint64_t ao = (uint64_t)(((kk >> 2) * G::QCHUNK + (kk & 3) * 32) >> 4);
+                    const uint64_t bo = (uint64_t)(((kk >> 2) * G::KCHUNK + (kk & 3) * 32) >> 4);
+                    mma_ss_w(tS, ad0 + ao, bd0 + bo, idesc_qk, kk > 0 ? 1u : 0u);
                 }
-                tc_commit(S_FULL(s));
-                if (t == K - 1) tc_commit(Q_EMPTY(s));
+                tc_commit_w(S_FULL(s));
+                if (t == K - 1) tc_commit_w(Q_EMPTY(s));
             };
             auto issue_pv = [&](int s, int t, uint32_t st) {
-                const uint32_t vb = sRing + st * G::TILE_BYTES;
+                // V tile as the MN-major B operand: 16 keys = 16 rows of 128 B; the second
+                // 64-wide chunk of d sits one KCHUNK further (LBO).
+                const uint64_t vd0 = sdesc_sw128(sRing + st * G::TILE_BYTES, G::KCHUNK, 1024);
                 const uint32_t tP = tbase + s * 256, tO = tbase + s * 256 + 128;
 #pragma unroll
-                for (int kk = 0; kk < B / 16; ++kk) {
-                    // V tile as the MN-major B operand: 16 keys = 16 rows of 128 B; the
-                    // second 64-wide chunk of d sits one KCHUNK further (LBO).
-                    const uint64_t bd = sdesc_sw128(vb + kk * 2048, G::KCHUNK, 1024);
-                    mma_ts(tO, tP + kk * 8, bd, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
-                }
-                if (t == K - 1) tc_commit(O_FULL(s));
+                for (int kk = 0; kk < B / 16; ++kk)
+                    mma_ts_w(tO, tP + kk * 8, vd0 + (uint64_t)((kk * 2048) >> 4), idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
+                if (t == K - 1) tc_commit_w(O_FULL(s));
             };
             for (int r = 0; r < rounds; ++r) {
                 uint32_t act_bits = 0;
@@ -357,12 +359,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const uint32_t pp = (pf_bits >> s) & 1u;
                         pf_bits ^= 1u << s;
                         TR(0, npv, 3);
-                        uint32_t okP, okV, okK;
-                        mbar_try_wait3(P_FULL(s), pp, RING_FULL(sv), vp, RING_FULL(more ? sk : sv), more ? kp : vp,
-                                       okP, okV, okK);
-                        if (!okP) mbar_wait(P_FULL(s), pp);
-                        if (!okV) mbar_wait(RING_FULL(sv), vp);
-                        if (more && !okK) mbar_wait(RING_FULL(sk), kp);
+                        // non-blocking probe of the group's barriers (test_wait: an incomplete
+                        // P_FULL must not put the thread to sleep), then wait for the rest
+                        const uint32_t ok = mbar_try_wait4(P_FULL(s), pp, RING_FULL(sv), vp,
+                                                           RING_FULL(more ? sk : sv), more ? kp : vp,
+                                                           RING_FULL(sv), vp);
+                        if (!(ok & 1u)) mbar_wait(P_FULL(s), pp);
+                        if (!(ok & 2u)) mbar_wait(RING_FULL(sv), vp);
+                        if (more && !(ok & 4u)) mbar_wait(RING_FULL(sk), kp);
                         TR(0, npv, 4);
                         tc_fence_after();
                         issue_pv(s, t, sv);
@@ -584,6 +588,11 @@ veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint1
                                const int32_t *idx, const uint32_t *mask, int Hh, int NT, int B, int d,
                                int kk, float scale, uint16_t *o, float *lse, cudaStream_t s)
 {
+    static const int sched = [] {
+        const char *e = getenv("VEDA_ATTN");
+        return (e && e[0] == '1' && e[1] == 'q') ? 1 : 0;
+    }();
+    if (sched == 1) return launch_sparse_attn_1q(q, k, v, idx, mask, Hh, NT, B, d, kk, scale, o, lse, s);
     if (B == 128 && d == 128) return attn::launch<128, 128>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
     if (B == 128 && d == 64) return attn::launch<128, 64>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
     if (B == 64 && d == 128) return attn::launch<64, 128>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);

@@ -48,6 +48,9 @@ veda_status launch_topk(const float *scores, int Hh, int NT, int k, int32_t *idx
 veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v,
                                const int32_t *idx, const uint32_t *mask, int Hh, int NT, int B, int d,
                                int kk, float scale, uint16_t *o, float *lse, cudaStream_t s);
+veda_status launch_sparse_attn_1q(const uint16_t *q, const uint16_t *k, const uint16_t *v, const int32_t *idx,
+                                  const uint32_t *mask, int Hh, int NT, int B, int d, int kk, float scale,
+                                  uint16_t *o, float *lse, cudaStream_t s);
 veda_status launch_target_scores(const uint16_t *q, const uint16_t *k, const uint32_t *mask, const float *lse,
                                  int Hh, int NT, int B, int d, float scale, float *out, cudaStream_t s);
 veda_status launch_permute_scalar(const float *x, int64_t hs, const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp,

@@ -61,6 +61,31 @@ __device__ __forceinline__ void mbar_try_wait3(uint32_t b0, uint32_t p0, uint32_
         : "r"(b0), "r"(p0), "r"(b1), "r"(p1), "r"(b2), "r"(p2)
         : "memory");
 }
+// Probe four mbarrier phases in one asm block without blocking (test_wait never suspends,
+// unlike try_wait, which sleeps up to a HW time limit on an incomplete phase); latencies
+// overlap.  Bit i of the result is set iff barrier i's phase is complete.
+__device__ __forceinline__ uint32_t mbar_try_wait4(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1, uint32_t b2,
+                                                   uint32_t p2, uint32_t b3, uint32_t p3)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred q0, q1, q2, q3;\n\t.reg .b32 t0, t1, t2, t3;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q0, [%1], %2;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q1, [%3], %4;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q2, [%5], %6;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q3, [%7], %8;\n\t"
+        "selp.u32 t0, 1, 0, q0;\n\t"
+        "selp.u32 t1, 2, 0, q1;\n\t"
+        "selp.u32 t2, 4, 0, q2;\n\t"
+        "selp.u32 t3, 8, 0, q3;\n\t"
+        "or.b32 t0, t0, t1;\n\t"
+        "or.b32 t2, t2, t3;\n\t"
+        "or.b32 %0, t0, t2;\n\t}"
+        : "=r"(ok)
+        : "r"(b0), "r"(p0), "r"(b1), "r"(p1), "r"(b2), "r"(p2), "r"(b3), "r"(p3)
+        : "memory");
+    return ok;
+}
 // Spin on an mbarrier phase.  A wait that never completes (a pipeline bug) traps
 // after ~2^26 polls instead of hanging the GPU, reporting the barrier it was stuck on.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
@@ -165,6 +190,42 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Warp-uniform variants: executed by ALL 32 lanes of the issuing warp with warp-uniform
+// operands; elect.sync picks one lane inside the asm.  Keeping the issue code convergent
+// lets ptxas hold descriptors / TMEM addresses in uniform registers instead of wrapping
+// every tcgen05 instruction in an ELECT + R2UR + branch loop (the divergent lane-0 form
+// costs ~80 clk per MMA, more than a 128x128x16 MMA takes to execute).
+__device__ __forceinline__ void mma_ss_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_w(uint32_t bar)
+{
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
         : "memory");
 }
 

@@ -358,3 +358,18 @@ def test_waver_full_size_sampled(V, oracle):
         check_attention(oracle, oq, ok_, ov, got, omask, u16(path.ot[h:h + 1]), units=units, tag=f"waver h{h}")
     # untiling of every head is the exact inverse of tiling
     assert torch.equal(V.tile_unpermute(path.qt, pre.lat, [pre.cfg]), q)
+
+
+def test_alt_schedule_1q_parity():
+    """The alternative one-query-tile schedule (csrc/attn_fwd_1q.cu, selected by VEDA_ATTN=1q
+    at library load) passes the same attention parity tests, in a fresh process."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, VEDA_ATTN="1q")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_parity.py"),
+                        "-k", "test_attention_vs_oracle or test_dense_k_equals_nt or test_random_lists_and_small_k or test_end_to_end_path_object"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
