@@ -12,8 +12,9 @@ the path; the step time is the max over ranks ("scaling": "strong", total work f
 Rank 0 prints ONE JSON line.  ``value`` is ms per call (lower is better).  Extra keys:
 speedup_vs_dense (same attention kernel with every tile kept, kernel-only, divided by
 the full sparse path), roofline of the attention kernel (executed FLOPs only),
-cpu_baseline (the fp64 oracle on a bounded sample, extrapolated), e2e (host buffers,
-H2D + path + D2H), gpu_launches (libveda's own launch counter over the timed region).
+cpu_baseline (the fp64 oracle on a bounded sample, extrapolated), e2e (pinned host
+buffers through veda_sparse_attention_host: H2D + path + D2H pipelined over head chunks),
+gpu_launches (libveda's own launch counter over the timed region).
 """
 from __future__ import annotations
 
@@ -294,14 +295,9 @@ def run_ours(args):
     if not args.no_e2e:
         qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
         oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-        qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-
+        # the C-ABI host entry point: H2D, the five steps and D2H pipelined over head chunks
         def e2e_step():
-            qd.copy_(qh, non_blocking=True)
-            kd.copy_(kh, non_blocking=True)
-            vd.copy_(vh, non_blocking=True)
-            path(qd, kd, vd, out=out)
-            oh.copy_(out, non_blocking=True)
+            path.run_host(qh, kh, vh, out=oh)
 
         e2e_step()
         barrier()
@@ -317,7 +313,9 @@ def run_ours(args):
         bo = out.numel() * out.element_size()
         e2e = {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": bi * world,
                "d2h_bytes_per_step": bo * world}
-        del qh, kh, vh, oh, qd, kd, vd
+        path._host_ws = None
+        path._host_ws_key = None
+        del qh, kh, vh, oh
 
     # optional Ulysses mode (N > 1): sequence-sharded inputs [N_r, Hh, d], all-to-all to
     # heads, local path, all-to-all back; its two exchanges are the only collectives

@@ -153,6 +153,38 @@ VEDA_API veda_status veda_tile_unpermute(const uint16_t *o_tiled, veda_latent la
                                 uint16_t *o, int64_t head_stride, int64_t token_stride,
                                 void *stream);
 
+/* ---- the whole path on HOST buffers (end-to-end call) ------------------------------ */
+
+/* Device workspace veda_sparse_attention_host needs (two buffer sets of one head chunk:
+ * token-layout Q/K/V/O, tiled Q/K/V/O, counts, masks, scores, index lists, scorer
+ * workspace).  heads_per_chunk <= 0 selects the default ceil(Hh/8).                   */
+VEDA_API veda_status veda_sparse_attention_host_workspace(veda_latent lat, const veda_tile_cfg *cfg /* host [Hh] */,
+                                                          int32_t Hh, int32_t d, int32_t k,
+                                                          const veda_scorer *w /* host */,
+                                                          int32_t heads_per_chunk, size_t *bytes /* host */);
+
+/* Steps 1-5 for Q/K/V in HOST memory, output to HOST memory: the call a DiT layer makes
+ * when its activations are not resident on the GPU.  Heads are independent (PAPER.md:270,
+ * Alg. 2), so the heads are processed in chunks of heads_per_chunk through
+ * two device buffer sets: the H2D copy of chunk c+1, the five steps on chunk c (on
+ * `stream`) and the D2H copy of chunk c-1 overlap (two library-owned side streams,
+ * ordered against `stream` by events).  Every chunk is tiled on the padded grid of the
+ * whole call, so o_host is bit-identical to veda_tile_permute .. veda_tile_unpermute on
+ * all Hh heads with the same k.
+ *   q_host, k_host, v_host, o_host : host bf16, dense [Hh][N][d] (head_stride = N*d,
+ *       token_stride = d) or dense [N][Hh][d] (head_stride = d, token_stride = Hh*d);
+ *       page-locked memory is needed for the copies to overlap.  The inputs are read and
+ *       o_host written asynchronously: valid only after `stream` is synchronised.
+ *   w : scorer weights of all Hh heads (device arrays, as for veda_tile_score)
+ *   workspace : device, >= veda_sparse_attention_host_workspace bytes, 16-byte aligned */
+VEDA_API veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k_host,
+                                                const uint16_t *v_host, int64_t head_stride,
+                                                int64_t token_stride, veda_latent lat,
+                                                const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh,
+                                                int32_t d, int32_t k, const veda_scorer *w /* host */,
+                                                int32_t heads_per_chunk, uint16_t *o_host, void *workspace,
+                                                size_t workspace_bytes, void *stream);
+
 /* ---- fused forms used by the composed path (same results as the unfused calls) ---- */
 
 /* veda_tile_permute + TripPool of the tiled tensor in ONE pass over HBM (the statistics

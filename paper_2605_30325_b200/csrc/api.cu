@@ -81,12 +81,6 @@ veda_status make_tmap_bf16(CUtensorMap *map, const void *base, uint64_t rows, ui
     return VEDA_OK;
 }
 
-namespace {
-
-struct Shape {
-    int Tp, Hp, Wp, B, NT;
-};
-
 veda_status check_arch()
 {
     static int ok_dev = -1;
@@ -102,14 +96,14 @@ veda_status check_arch()
     return VEDA_OK;
 }
 
-int lcm_int(int a, int b)
+static int lcm_int(int a, int b)
 {
     int x = a, y = b;
     while (y) { const int t = x % y; x = y; y = t; }
     return a / x * b;
 }
 
-bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+static bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 
 veda_status shape_of(veda_latent lat, const veda_tile_cfg *cfg, int Hh, Shape *sh, HeadCfgs *hc)
 {
@@ -140,9 +134,11 @@ veda_status shape_of(veda_latent lat, const veda_tile_cfg *cfg, int Hh, Shape *s
     return VEDA_OK;
 }
 
-inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
-
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+namespace {
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 }  // namespace
 }  // namespace veda

@@ -30,6 +30,14 @@ struct HeadCfgs {
     uint8_t pt[kMaxHeads], ph[kMaxHeads], pw[kMaxHeads];
 };
 
+// padded grid of a call (readings R4/R5): per-axis lcm of the heads' tile extents
+struct Shape {
+    int Tp, Hp, Wp, B, NT;
+};
+veda_status check_arch();
+veda_status shape_of(veda_latent lat, const veda_tile_cfg *cfg, int Hh, Shape *sh, HeadCfgs *hc);
+size_t align256(size_t v);
+
 // launchers (defined in the per-kernel .cu files)
 veda_status launch_tile_permute(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfgs &cf, int Hh,
                                 int Tp, int Hp, int Wp, int T, int H, int W, int B, int NT, int d,

@@ -12,6 +12,9 @@
 // construction and identical to "sort by (S desc, j asc), take k, sort by j".
 #include "common.cuh"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace veda {
 namespace {
 
@@ -110,10 +113,87 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const float *__restric
     }
 }
 
+
+// Warp-per-row variant for n_tiles <= 32*C: lane l holds keys j = 32*i + l (i < C) in
+// registers.  The k-th largest key T is built bit by bit from the MSB: a candidate bit is
+// kept while at least k keys are >= the candidate (one compare per key plus a redux.sync
+// per bit); the search stops as soon as exactly k keys are >= the candidate.  The index-
+// order pass then takes keys > T plus the first (k - #{> T}) keys == T, compacted by
+// ballots over i -- the same contract as topk_kernel above, without smem or CTA syncs.
+constexpr int TKW_WARPS = 8;
+
+template <int C>
+__global__ void __launch_bounds__(TKW_WARPS * 32) topk_warp_kernel(const float *__restrict__ S, int rows, int NT,
+                                                                   int k, int32_t *__restrict__ idx)
+{
+    const int lane = threadIdx.x & 31;
+    const int row = blockIdx.x * TKW_WARPS + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const float *s = S + (size_t)row * NT;
+    uint32_t key[C];
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+        const int j = 32 * i + lane;
+        key[i] = j < NT ? order_key(__ldg(s + j)) : 0u;  // 0 sorts below every finite or -inf key
+    }
+    const uint32_t kk = (uint32_t)k;
+    uint32_t T = 0;
+#pragma unroll 1
+    for (int b = 31; b >= 0; --b) {
+        const uint32_t c = T | (1u << b);
+        uint32_t n = 0;
+#pragma unroll
+        for (int i = 0; i < C; ++i) n += key[i] >= c;
+        n = __reduce_add_sync(0xFFFFFFFFu, n);
+        if (n >= kk) {
+            T = c;
+            if (n == kk) break;  // {key >= T} is exactly the answer
+        }
+    }
+    uint32_t ngt = 0;
+#pragma unroll
+    for (int i = 0; i < C; ++i) ngt += key[i] > T;
+    ngt = __reduce_add_sync(0xFFFFFFFFu, ngt);
+    const uint32_t need = kk - ngt;  // keys == T to take, lowest indices first
+    const uint32_t lt = (1u << lane) - 1u;
+    int32_t *out = idx + (size_t)row * k;
+    uint32_t base = 0, eq_seen = 0;
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+        const int j = 32 * i + lane;
+        const bool eq = j < NT && key[i] == T;
+        const uint32_t beq = __ballot_sync(0xFFFFFFFFu, eq);
+        const bool sel = (j < NT && key[i] > T) || (eq && eq_seen + __popc(beq & lt) < need);
+        eq_seen += __popc(beq);
+        const uint32_t bsel = __ballot_sync(0xFFFFFFFFu, sel);
+        if (sel) out[base + __popc(bsel & lt)] = j;
+        base += __popc(bsel);
+    }
+}
+
 }  // namespace
+
+template <int C>
+static veda_status launch_topk_warp(const float *scores, int rows, int NT, int k, int32_t *idx, cudaStream_t s)
+{
+    topk_warp_kernel<C><<<(rows + TKW_WARPS - 1) / TKW_WARPS, TKW_WARPS * 32, 0, s>>>(scores, rows, NT, k, idx);
+    count_launch();
+    return check_launch("select_topk");
+}
 
 veda_status launch_topk(const float *scores, int Hh, int NT, int k, int32_t *idx, cudaStream_t s)
 {
+    const int rows = Hh * NT;
+    static const bool force_cta = [] {
+        const char *e = getenv("VEDA_TOPK");
+        return e && !strcmp(e, "cta");
+    }();
+    if (!force_cta) {
+        if (NT <= 32 * 4) return launch_topk_warp<4>(scores, rows, NT, k, idx, s);
+        if (NT <= 32 * 16) return launch_topk_warp<16>(scores, rows, NT, k, idx, s);
+        if (NT <= 32 * 32) return launch_topk_warp<32>(scores, rows, NT, k, idx, s);
+        if (NT <= 32 * 64) return launch_topk_warp<64>(scores, rows, NT, k, idx, s);
+    }
     const size_t smem = (size_t)NT * sizeof(uint32_t);
     if (smem > 200 * 1024) return fail(VEDA_ERR_SHAPE, "select_topk: n_tiles=%d too large", NT);
     static size_t attr = 0;
@@ -123,7 +203,7 @@ veda_status launch_topk(const float *scores, int Hh, int NT, int k, int32_t *idx
         if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
         attr = smem;
     }
-    topk_kernel<<<Hh * NT, TK_THREADS, smem, s>>>(scores, NT, k, idx);
+    topk_kernel<<<rows, TK_THREADS, smem, s>>>(scores, NT, k, idx);
     count_launch();
     return check_launch("select_topk");
 }

@@ -29,7 +29,7 @@ EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_worksp
            "veda_trippool", "veda_project", "veda_pair_scores", "veda_status_str", "veda_last_error",
            "veda_launch_count", "veda_check_device", "veda_tile_permute_pool", "veda_tile_score_pooled",
            "veda_target_scores", "veda_tile_recall", "veda_tile_permute_scalar", "veda_tile_unpermute_scalar",
-           "veda_sq_err"]
+           "veda_sq_err", "veda_sparse_attention_host_workspace", "veda_sparse_attention_host"]
 
 
 class VedaError(RuntimeError):
@@ -86,6 +86,8 @@ def load(path: str = LIB_PATH):
         "veda_tile_permute_scalar": ([P, i64, Latent, P, i32, f32, P, P], i32),
         "veda_tile_unpermute_scalar": ([P, Latent, P, i32, P, i64, P], i32),
         "veda_sq_err": ([P, P, i64, i64, i32, P, P], i32),
+        "veda_sparse_attention_host_workspace": ([Latent, P, i32, i32, i32, P, i32, P], i32),
+        "veda_sparse_attention_host": ([P, P, P, i64, i64, Latent, P, i32, i32, i32, P, i32, P, P, sz, P], i32),
         "veda_status_str": ([i32], ctypes.c_char_p),
         "veda_last_error": ([], ctypes.c_char_p),
         "veda_launch_count": ([], ctypes.c_uint64),
@@ -449,18 +451,51 @@ class SparseAttention:
 
     LAUNCHES_PER_CALL = 3 + 2 + 4 + 1 + 1 + 1 + 1  # permute x3, pool x2, mlp 2x2, scores, topk, attn, unpermute
 
+    def run_host(self, q, k, v, out=None, heads_per_chunk: int = 0):
+        """The same call on HOST tensors (veda_sparse_attention_host): q, k, v, out are
+        pinned CPU bf16 tensors, dense [Hh, N, d] or dense views [N, Hh, d] permuted to
+        [Hh, N, d]; the library pipelines H2D / the five steps / D2H over head chunks.
+        Returns ``out`` (valid once the current stream is synchronised)."""
+        lib, s = load(), _stream()
+        Hh, d = self.Hh, self.d
+        N = self.lat[0] * self.lat[1] * self.lat[2]
+        for t in (q, k, v):
+            if t.is_cuda or t.dtype != torch.bfloat16 or tuple(t.shape) != (Hh, N, d):
+                raise VedaError("run_host: q/k/v must be CPU bf16 [Hh, N, d]")
+            if t.stride() != q.stride():
+                raise VedaError("run_host: q/k/v must share one layout")
+        if out is None:
+            out = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, pin_memory=True)
+        if out.stride() != q.stride():
+            raise VedaError("run_host: out must have the layout of q")
+        lat, cfg = Latent(*self.lat), _cfg_array(self.cfgs, Hh)
+        key = (heads_per_chunk,)
+        if getattr(self, "_host_ws_key", None) != key:
+            nb = ctypes.c_size_t(0)
+            _check(lib.veda_sparse_attention_host_workspace(lat, cfg, Hh, d, self.k, ctypes.byref(self.scorer),
+                                                            heads_per_chunk, ctypes.byref(nb)),
+                   "sparse_attention_host_workspace")
+            self._host_ws = torch.empty(nb.value, dtype=torch.uint8, device=self.qt.device)
+            self._host_ws_key = key
+        _check(lib.veda_sparse_attention_host(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat, cfg, Hh, d,
+                                              self.k, ctypes.byref(self.scorer), heads_per_chunk, _ptr(out),
+                                              _ptr(self._host_ws), self._host_ws.numel(), s),
+               "sparse_attention_host")
+        return out
+
 
 def sparse_attention(q, k, v, lat, cfgs, scorer_weights, sparsity=None, k_keep=None):
     """One-shot convenience: the five steps on [Hh, N, d] bf16 CUDA views -> o [Hh, N, d].
 
-    CPU (pinned) inputs are copied to the current device first and the output is
-    copied back, so the same call measures the end-to-end path."""
-    host = not q.is_cuda
-    if host:
-        dev = torch.device("cuda")
-        q, k, v = (t.to(dev, non_blocking=True) for t in (q, k, v))
-        scorer_weights = {n: w.to(dev, non_blocking=True) for n, w in scorer_weights.items()}
+    CPU (pinned) inputs go through veda_sparse_attention_host (H2D, the five steps and
+    D2H pipelined over head chunks) and the output is returned on the host."""
     Hh, N, d = q.shape
+    if not q.is_cuda:  # host tensors: the pipelined end-to-end entry point
+        dev = torch.device("cuda")
+        scorer_weights = {n: w.to(dev) for n, w in scorer_weights.items()}
+        path = SparseAttention(lat, cfgs, Hh, d, scorer_weights, sparsity=sparsity, k=k_keep, device=dev)
+        o = path.run_host(q, k, v)
+        torch.cuda.current_stream().synchronize()
+        return o
     path = SparseAttention(lat, cfgs, Hh, d, scorer_weights, sparsity=sparsity, k=k_keep, device=q.device)
-    o = path(q, k, v)
-    return o.cpu() if host else o
+    return path(q, k, v)

@@ -373,3 +373,51 @@ def test_alt_schedule_1q_parity():
                         "-k", "test_attention_vs_oracle or test_dense_k_equals_nt or test_random_lists_and_small_k or test_end_to_end_path_object"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("NT,k", [(1, 1), (7, 3), (33, 32), (128, 5), (336, 34), (700, 36), (1920, 96),
+                                  (2048, 2048), (2049, 100), (4880, 96)])
+def test_topk_sizes_and_ties_bit_exact(V, oracle, NT, k):
+    """Both select kernels (warp-per-row for n_tiles <= 2048, CTA-per-row above) against the
+    oracle's sort-based top-k (R10/R11/R16): quantised scores give long runs of exact ties,
+    -inf columns (empty key tiles) and -0.0 / +0.0 pairs."""
+    g = torch.Generator().manual_seed(NT * 131 + k)
+    Hh = 3
+    s = torch.randint(-6, 7, (Hh, NT, NT), generator=g).float() / 4.0
+    s[0] = torch.randn(NT, NT, generator=g)  # head 0: (almost surely) distinct scores
+    s[1, :, ::5] = float("-inf")
+    s[2, :, ::3] = -0.0
+    idx = V.select_topk(s.cuda(), k).cpu().numpy()
+    want = oracle.topk(s.numpy().astype(np.float64), k)
+    assert np.array_equal(idx, want)
+
+
+@pytest.mark.parametrize("layout,chunk", [("hnd", 0), ("hnd", 3), ("nhd", 2), ("nhd", 1)])
+def test_host_pipeline_bit_identical(V, layout, chunk):
+    """veda_sparse_attention_host (H2D / path / D2H pipelined over head chunks, every chunk
+    tiled on the whole call's padded grid) equals the device path on all heads bit for bit:
+    mixed per-head configs (so a chunk's own lcm grid would differ), uneven last chunk."""
+    c = Case("mixed_cfgs", **CASES["mixed_cfgs"])
+    dev = torch.device("cuda")
+    w = {n: t.to(dev) for n, t in c.w.items()}
+    path = V.SparseAttention(c.lat, c.cfgs, c.Hh, c.d, w, k=c.k_keep, device=dev)
+    want = path(c.q.to(dev), c.k.to(dev), c.v.to(dev)).cpu()
+    if layout == "hnd":
+        qh, kh, vh = (t.contiguous().pin_memory() for t in (c.q, c.k, c.v))
+    else:  # dense [N, Hh, d] viewed as [Hh, N, d]
+        qh, kh, vh = (t.transpose(0, 1).contiguous().pin_memory().transpose(0, 1) for t in (c.q, c.k, c.v))
+    for _ in range(2):  # second call reuses the cached workspace and side streams
+        got = path.run_host(qh, kh, vh, heads_per_chunk=chunk)
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+
+
+def test_host_pipeline_one_shot_api(V):
+    """veda.sparse_attention on CPU tensors routes through the host pipeline."""
+    c = Case("toy_b128", **CASES["toy_b128"])
+    dev = torch.device("cuda")
+    got = V.sparse_attention(c.q, c.k, c.v, c.lat, c.cfgs, c.w, k_keep=c.k_keep)
+    assert not got.is_cuda
+    want = V.sparse_attention(c.q.to(dev), c.k.to(dev), c.v.to(dev), c.lat, c.cfgs,
+                              {n: t.to(dev) for n, t in c.w.items()}, k_keep=c.k_keep).cpu()
+    assert torch.equal(got.view(torch.int16), want.view(torch.int16))
