@@ -92,17 +92,37 @@ struct Geo {
 #endif
 constexpr int EMU_EVERY = VEDA_EMU_EVERY;
 
-// 2^x for x <= ~8: 2^x = 2^n * 2^f, n = rint(x) by the 1.5*2^23 trick, f in [-1/2, 1/2],
-// 2^f by a cubic (max rel. error 7.5e-5, far below the bf16 rounding of P, 2^-9).
-__device__ __forceinline__ float ex2_emu(float x)
+// 2^x for a PAIR on the FMA/ALU pipes with packed fp32x2 arithmetic (10 issue slots for
+// two results, no MUFU): clamp (FMNMX x2), n = rint(x) via the 1.5*2^23 trick and
+// f = x - n (FADD2 x3), cubic 2^f (FFMA2 x3, max rel. error 7.5e-5 << bf16's 2^-9),
+// exponent insertion (LEA x2).  x = -inf (masked keys) gives ~2^-125 ~ 0.
+__device__ __forceinline__ void ex2_emu2(float &y0, float &y1, float x0, float x1)
 {
-    x = fmaxf(x, -125.0f);
-    const float j = x + 12582912.0f;
-    const float f = x - (j - 12582912.0f);
-    float p = fmaf(f, 0.05517162f, 0.24261113f);
-    p = fmaf(p, f, 0.69326097f);
-    p = fmaf(p, f, 0.99992806f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
+    x0 = fmaxf(x0, -125.0f);  // 2^n * p must stay a normal number (p in [0.7, 1.42))
+    x1 = fmaxf(x1, -125.0f);
+    float j0, j1, t0, t1, f0, f1, p0, p1;
+    asm("{\n\t.reg .b64 rx, rm, rj, rt, rf, rp, c3, c2, c1, c0;\n\t"
+        "mov.b64 rx, {%8, %9};\n\t"
+        "mov.b64 rm, {%10, %10};\n\t"
+        "add.rn.f32x2 rj, rx, rm;\n\t"
+        "sub.rn.f32x2 rt, rj, rm;\n\t"
+        "sub.rn.f32x2 rf, rx, rt;\n\t"
+        "mov.b64 c3, {%11, %11};\n\t"
+        "mov.b64 c2, {%12, %12};\n\t"
+        "mov.b64 c1, {%13, %13};\n\t"
+        "mov.b64 c0, {%14, %14};\n\t"
+        "fma.rn.f32x2 rp, rf, c3, c2;\n\t"
+        "fma.rn.f32x2 rp, rp, rf, c1;\n\t"
+        "fma.rn.f32x2 rp, rp, rf, c0;\n\t"
+        "mov.b64 {%0, %1}, rj;\n\t"
+        "mov.b64 {%2, %3}, rt;\n\t"
+        "mov.b64 {%4, %5}, rf;\n\t"
+        "mov.b64 {%6, %7}, rp;\n\t}"
+        : "=f"(j0), "=f"(j1), "=f"(t0), "=f"(t1), "=f"(f0), "=f"(f1), "=f"(p0), "=f"(p1)
+        : "f"(x0), "f"(x1), "f"(12582912.0f), "f"(0.05517162f), "f"(0.24261113f), "f"(0.69326097f),
+          "f"(0.99992806f));
+    y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(j0) << 23));
+    y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(j1) << 23));
 }
 
 // packed fp32x2 (sm_100): (d0, d1) = (a0, a1) * b + c
@@ -467,8 +487,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         ffma2_bc(x0, x1, u2f(sr[c][e]), u2f(sr[c][e + 1]), sl2, -mu);
                         float a, b;
                         if (EMU_EVERY > 0 && (i % EMU_EVERY) == EMU_EVERY - 1) {
-                            a = ex2_emu(x0);  // FMA-pipe polynomial: unloads the MUFU unit
-                            b = ex2_emu(x1);
+                            ex2_emu2(a, b, x0, x1);  // FMA-pipe polynomial: unloads the MUFU unit
                         } else {
                             a = ex2(x0);
                             b = ex2(x1);

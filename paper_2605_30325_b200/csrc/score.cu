@@ -18,28 +18,41 @@ namespace {
 
 // ---------------------------------------------------------------- TripPool
 // One CTA of 128 threads per (head, tile).  Thread = (row group, 8-channel chunk);
-// 16-byte loads; fp64 sums, exact fp32 max/min; partials reduced through smem.
-template <int D>
+// all of a thread's rows are loaded (16-byte, predicated on the slot mask) before any
+// arithmetic so B/RG loads are in flight per thread; fp64 sums, exact fp32 max/min;
+// partials reduced through smem.
+template <int D, int BT>
 __global__ void __launch_bounds__(128) trippool_kernel(const uint16_t *__restrict__ xt,
-                                                       const uint32_t *__restrict__ mask, int B,
+                                                       const uint32_t *__restrict__ mask,
                                                        float *__restrict__ z)
 {
     constexpr int CH = D / 8;       // chunks per row
     constexpr int RG = 128 / CH;    // row groups
+    constexpr int RPT = BT / RG;    // rows per thread
+    constexpr int MW = BT / 32;
     const int ti = blockIdx.x;
     const int c8 = threadIdx.x % CH, rg = threadIdx.x / CH;
-    const int MW = B / 32;
     const uint32_t *mk = mask + (size_t)ti * MW;
-    const uint4 *src = reinterpret_cast<const uint4 *>(xt + (size_t)ti * B * D);
+    const uint4 *src = reinterpret_cast<const uint4 *>(xt + (size_t)ti * BT * D);
+    uint32_t mw[MW];
+#pragma unroll
+    for (int i = 0; i < MW; ++i) mw[i] = __ldg(mk + i);
+    uint4 v[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int r = rg + i * RG;
+        v[i] = ((mw[r >> 5] >> (r & 31)) & 1u) ? __ldg(src + (size_t)r * CH + c8) : make_uint4(0, 0, 0, 0);
+    }
     double sum[8];
     float mx[8], mn[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) { sum[q] = 0.0; mx[q] = -INFINITY; mn[q] = INFINITY; }
     int n = 0;
-    for (int r = rg; r < B; r += RG) {
-        if (!((__ldg(mk + (r >> 5)) >> (r & 31)) & 1u)) continue;
-        const uint4 v = __ldg(src + (size_t)r * CH + c8);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int r = rg + i * RG;
+        if (!((mw[r >> 5] >> (r & 31)) & 1u)) continue;
+        const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const float lo = __uint_as_float(w[q] << 16), hi = __uint_as_float(w[q] & 0xFFFF0000u);
@@ -395,12 +408,16 @@ veda_status launch_trippool(const uint16_t *xt, const uint32_t *mask, int Hh, in
                             float *z, cudaStream_t s)
 {
     const int blocks = Hh * NT;
-    if (d == 128)
-        trippool_kernel<128><<<blocks, 128, 0, s>>>(xt, mask, B, z);
-    else if (d == 64)
-        trippool_kernel<64><<<blocks, 128, 0, s>>>(xt, mask, B, z);
+    if (d == 128 && B == 128)
+        trippool_kernel<128, 128><<<blocks, 128, 0, s>>>(xt, mask, z);
+    else if (d == 128 && B == 64)
+        trippool_kernel<128, 64><<<blocks, 128, 0, s>>>(xt, mask, z);
+    else if (d == 64 && B == 128)
+        trippool_kernel<64, 128><<<blocks, 128, 0, s>>>(xt, mask, z);
+    else if (d == 64 && B == 64)
+        trippool_kernel<64, 64><<<blocks, 128, 0, s>>>(xt, mask, z);
     else
-        return fail(VEDA_ERR_SHAPE, "trippool: unsupported d=%d", d);
+        return fail(VEDA_ERR_SHAPE, "trippool: unsupported B=%d d=%d", B, d);
     count_launch();
     return check_launch("trippool");
 }

@@ -28,13 +28,13 @@ def main():
     w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, heads=heads).items()}
     path = veda.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev)
     path(q, k, v)
-    tr = torch.zeros(4 * 128 * 8, dtype=torch.int64, device=dev)
+    tr = torch.zeros(16 * 128 * 8, dtype=torch.int64, device=dev)
     lib.veda_dbg_set_attn_trace(ctypes.c_void_p(tr.data_ptr()))
     veda.sparse_attn_fwd(path.qt, path.kt, path.vt, path.idx, path.mask)  # warm
     tr.zero_()
     veda.sparse_attn_fwd(path.qt, path.kt, path.vt, path.idx, path.mask)
     torch.cuda.synchronize()
-    t = tr.view(4, 128, 8).cpu().numpy().astype(np.int64)
+    t = tr.view(16, 128, 8).cpu().numpy().astype(np.int64)
     t0 = t[t > 0].min()
     t = np.where(t > 0, t - t0, -1)
     for role, name in ((0, "thread (both slots)"),):
@@ -43,15 +43,22 @@ def main():
             print(f"  n={n:3d} qk {t[role, n, 0]:8d} {t[role, n, 1]:8d} {t[role, n, 2]:8d} | "
                   f"pv {t[role, n, 3]:8d} {t[role, n, 4]:8d} {t[role, n, 5]:8d}")
     for s in (0, 1):
+        for qq in range(4):
+            r = t[1 + 4 * s + qq, 4:a.steps]
+            print(f"slot {s} quarter {qq}: wait-for-S {np.mean(r[:, 1] - r[:, 0]):.0f}, ld {np.mean(r[:, 2] - r[:, 1]):.0f}, "
+                  f"max {np.mean(r[:, 3] - r[:, 2]):.0f}, exp+st {np.mean(r[:, 4] - r[:, 3]):.0f}, "
+                  f"P_arrive - S_ok {np.mean(r[:, 5] - r[:, 1]):.0f}, P_arrive rel. to quarter 0 "
+                  f"{np.mean(r[:, 5] - t[1 + 4 * s, 4:a.steps, 5]):.0f}")
+    for s in (0, 1):
         print(f"slot {s} softmax (warp lane 0): wait_S_start, S_ok, ld_done, max_done, exp_st_done, P_arrive | "
               "dS_wait dLd dMax dExp dArr")
         for n in range(a.steps):
-            r = t[1 + s, n]
+            r = t[1 + 4 * s, n]
             d = [r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4]]
             print(f"  t={n:3d} {r[0]:8d} {r[1]:8d} {r[2]:8d} {r[3]:8d} {r[4]:8d} {r[5]:8d} | " + " ".join(f"{x:6d}" for x in d))
     # steady-state averages
     for s in (0, 1):
-        r = t[1 + s, 4:a.steps]
+        r = t[1 + 4 * s, 4:a.steps]
         per = np.diff(r[:, 1]).mean()
         print(f"slot {s}: mean period between S arrivals {per:.0f} clk; mean wait-for-S {np.mean(r[:, 1] - r[:, 0]):.0f}, "
               f"ld {np.mean(r[:, 2] - r[:, 1]):.0f}, max {np.mean(r[:, 3] - r[:, 2]):.0f}, exp+st {np.mean(r[:, 4] - r[:, 3]):.0f}, "
