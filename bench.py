@@ -4,8 +4,9 @@
                     [--sparsity S] [--regime path|random] [--impl reference]
 
 One "step" = one sparse-attention call of a DiT layer: all five steps of the path
-(tile_permute x3 -> tile_score -> select_topk -> sparse_attn_fwd -> tile_unpermute) for
-every head of the workload, inputs already resident in HBM.  With N GPUs (torchrun)
+in its token-layout form (tile_pool Q/K -> tile_score_pooled -> select_topk ->
+sparse_attn_fwd_tokens, which reads tiles from and writes rows to token order) for every
+head of the workload, inputs already resident in HBM.  With N GPUs (torchrun)
 heads are sharded (rank r owns heads [r*Hh/N, (r+1)*Hh/N)); there is no collective in
 the path; the step time is the max over ranks ("scaling": "strong", total work fixed).
 
@@ -238,23 +239,23 @@ def run_ours(args):
     launches = veda.launch_count() - n0
     total_ms = start.elapsed_time(stop)
     ms_step_local = total_ms / args.steps
-    parts = {"permute": 0.0, "score": 0.0, "topk": 0.0, "attn": 0.0, "unpermute": 0.0}
+    parts = {n: 0.0 for n in path.STEPS[path.mode]}
     for e in evs:
         for j, name in enumerate(parts):
             parts[name] += e[j].elapsed_time(e[j + 1]) / args.steps
+    if path.mode == "tokens":  # the token-layout attention stores rows straight to token order
+        parts["attn"] += parts.pop("untile")
     ms_step = shard.max_over_ranks(ms_step_local)
     attn_ms = shard.max_over_ranks(parts["attn"])
 
     # dense baseline: the same attention kernel with every tile kept (k = N_T), kernel only
     idx_dense = torch.arange(NT, dtype=torch.int32, device=dev).expand(Hh, NT, NT).contiguous()
-    dense_out = torch.empty_like(path.ot)
+    dense_out = torch.empty_like(out)
 
     def dense():
-        veda.sparse_attn_fwd(path.qt, path.kt, path.vt, idx_dense, path.mask, out=dense_out)
+        veda.sparse_attn_fwd_tokens(q, k, v, pre.lat, [pre.cfg], idx_dense, path.mask, out=dense_out)
 
-    # warm-up dense call doubles as pass 1 of the oracle tile mask (Eq. 4): row lse
-    _, lse_dense = veda.sparse_attn_fwd(path.qt, path.kt, path.vt, idx_dense, path.mask, out=dense_out,
-                                        want_lse=True)
+    dense()
     barrier()
     d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     d0.record(stream)
@@ -263,28 +264,33 @@ def run_ours(args):
     d1.record(stream)
     barrier()
     dense_ms = shard.max_over_ranks(d0.elapsed_time(d1) / args.dense_steps)
-    del idx_dense, dense_out
 
-    # recall (Eq. 3) of the path's kept lists against the oracle mask M~* = TopK(S_tgt),
-    # S_tgt from veda_target_scores (Eq. 4 pass 2); untimed, quality context only
+    # recall (Eq. 3) of the path's kept lists against the oracle mask M~* = TopK(S_tgt):
+    # pass 1 = the dense kernel's lse, pass 2 = veda_target_scores (Eq. 4) on tiled copies;
+    # untimed, quality context only
+    qt, kt, _ = path.tiled(q, k, q)
+    _, lse_dense = veda.sparse_attn_fwd_tokens(q, k, v, pre.lat, [pre.cfg], idx_dense, path.mask, out=dense_out,
+                                               want_lse=True)
+    del idx_dense, dense_out
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    s_tgt = veda.target_scores(path.qt, path.kt, path.mask, lse_dense)
+    s_tgt = veda.target_scores(qt, kt, path.mask, lse_dense)
     t1.record(stream)
     idx_star = veda.select_topk(s_tgt, kk)
     recall = veda.tile_recall(path.idx, idx_star, path.cnt).item()
     target_ms = shard.max_over_ranks(t0.elapsed_time(t1))
-    del s_tgt, idx_star, lse_dense
+    del s_tgt, idx_star, lse_dense, qt, kt
+    torch.cuda.empty_cache()
 
     # attention kernel with uniformly random lists (regime R2, L2 worst case)
     ridx = synth.random_index_lists(Hh, NT, kk, seed_parts=("R2", args.workload, heads.start)).to(dev)
-    r_out = torch.empty_like(path.ot)
-    veda.sparse_attn_fwd(path.qt, path.kt, path.vt, ridx, path.mask, out=r_out)
+    r_out = torch.empty_like(out)
+    veda.sparse_attn_fwd_tokens(q, k, v, pre.lat, [pre.cfg], ridx, path.mask, out=r_out)
     barrier()
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     r0.record(stream)
     for _ in range(max(1, args.steps // 2)):
-        veda.sparse_attn_fwd(path.qt, path.kt, path.vt, ridx, path.mask, out=r_out)
+        veda.sparse_attn_fwd_tokens(q, k, v, pre.lat, [pre.cfg], ridx, path.mask, out=r_out)
     r1.record(stream)
     barrier()
     rand_attn_ms = shard.max_over_ranks(r0.elapsed_time(r1) / max(1, args.steps // 2))

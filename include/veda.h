@@ -153,6 +153,35 @@ VEDA_API veda_status veda_tile_unpermute(const uint16_t *o_tiled, veda_latent la
                                 uint16_t *o, int64_t head_stride, int64_t token_stride,
                                 void *stream);
 
+/* ---- the path straight on the token layout (no tiled copies) ---- */
+
+/* TripPool of every tile of x, read straight from the token tensor (Alg. 2,
+ * Eq. 5): z [Hh][N_T][3d] fp32 exactly as veda_tile_permute + veda_trippool compute it
+ * (bit-identical), plus tile_count [Hh][N_T] and slot_mask [Hh][N_T][B/32] as
+ * veda_tile_permute writes them (either may be NULL).  x, strides: as veda_tile_permute. */
+VEDA_API veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int64_t token_stride,
+                                    veda_latent lat, const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh,
+                                    int32_t d, float *z, int32_t *tile_count, uint32_t *slot_mask, void *stream);
+
+/* Step 4 + step 5 on the token layout: Eq. 2 for every (head, query
+ * tile), the query tile and the kept key / value tiles fetched straight from q, k, v in
+ * token order by one TMA box per tile (padded slots zero-filled, reading R4), and each
+ * output row stored straight to its token (UnTile).  Bit-identical to
+ * veda_tile_permute x3 -> veda_sparse_attn_fwd -> veda_tile_unpermute.
+ *   q, k, v : token tensors sharing head_stride / token_stride (elements, multiples of 8,
+ *             head_stride != token_stride)
+ *   idx [Hh][N_T][k_keep], slot_mask [Hh][N_T][B/32] : as for veda_sparse_attn_fwd
+ *   o       : token tensor (o_head_stride, o_token_stride); rows of padded slots are not
+ *             written;  lse : [Hh][N_T][B] fp32 (tiled order) or NULL.
+ * Heads of one call may use any tile shapes (at most 8 distinct shapes per kernel launch;
+ * larger sets are split into several launches).                                         */
+VEDA_API veda_status veda_sparse_attn_fwd_tokens(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                                                 int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                                 const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh, int32_t d,
+                                                 const int32_t *idx, const uint32_t *slot_mask, int32_t k_keep,
+                                                 float softmax_scale, uint16_t *o, int64_t o_head_stride,
+                                                 int64_t o_token_stride, float *lse, void *stream);
+
 /* ---- the whole path on HOST buffers (end-to-end call) ------------------------------ */
 
 /* Device workspace veda_sparse_attention_host needs (two buffer sets of one head chunk:

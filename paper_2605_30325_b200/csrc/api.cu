@@ -81,6 +81,32 @@ veda_status make_tmap_bf16(CUtensorMap *map, const void *base, uint64_t rows, ui
     return VEDA_OK;
 }
 
+veda_status make_tmap_tile_tokens(CUtensorMap *map, const void *base, int64_t head_stride, int64_t token_stride,
+                                  int Hh, int T, int H, int W, int d, int pt, int ph, int pw, int *tok_major)
+{
+    auto fn = encode_fn();
+    if (!fn) return fail(VEDA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const bool tm = head_stride < token_stride;  // [N][Hh][d]-like: heads inside a token
+    cuuint64_t dims[5], strides[4];
+    cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+    const cuuint64_t ts = (cuuint64_t)token_stride * 2, hs = (cuuint64_t)head_stride * 2;
+    if (!tm) {  // d, W, H, T, Hh
+        dims[0] = d; dims[1] = W; dims[2] = H; dims[3] = T; dims[4] = Hh;
+        strides[0] = ts; strides[1] = ts * W; strides[2] = ts * W * H; strides[3] = hs;
+        box[0] = 64; box[1] = pw; box[2] = ph; box[3] = pt; box[4] = 1;
+    } else {    // d, Hh, W, H, T
+        dims[0] = d; dims[1] = Hh; dims[2] = W; dims[3] = H; dims[4] = T;
+        strides[0] = hs; strides[1] = ts; strides[2] = ts * W; strides[3] = ts * W * H;
+        box[0] = 64; box[1] = 1; box[2] = pw; box[3] = ph; box[4] = pt;
+    }
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(VEDA_ERR_CUDA, "cuTensorMapEncodeTiled (5-D tile box) failed (%d)", (int)r);
+    *tok_major = tm ? 1 : 0;
+    return VEDA_OK;
+}
+
 veda_status check_arch()
 {
     static int ok_dev = -1;
@@ -350,6 +376,47 @@ veda_status veda_sparse_attn_fwd(const uint16_t *q_tiled, const uint16_t *k_tile
     const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)d);
     return launch_sparse_attn(q_tiled, k_tiled, v_tiled, idx, slot_mask, Hh, n_tiles, B, d, k, scale, o_tiled, lse,
                               S(stream));
+}
+
+veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
+                           const veda_tile_cfg *cfg, int32_t Hh, int32_t d, float *z, int32_t *tile_count,
+                           uint32_t *slot_mask, void *stream)
+{
+    if (!x || !z) return fail(VEDA_ERR_NULL, "tile_pool: NULL pointer");
+    if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "tile_pool: d=%d unsupported", d);
+    if (!aligned16(x) || (head_stride % 8) || (token_stride % 8))
+        return fail(VEDA_ERR_ALIGN, "tile_pool: pointer/strides must be 16-byte aligned");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    Shape sh;
+    HeadCfgs hc;
+    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    return launch_tile_pool_tokens(x, head_stride, token_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
+                                   sh.NT, d, z, tile_count, slot_mask, S(stream));
+}
+
+veda_status veda_sparse_attn_fwd_tokens(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t head_stride,
+                                        int64_t token_stride, veda_latent lat, const veda_tile_cfg *cfg, int32_t Hh,
+                                        int32_t d, const int32_t *idx, const uint32_t *slot_mask, int32_t k_keep,
+                                        float softmax_scale, uint16_t *o, int64_t o_head_stride,
+                                        int64_t o_token_stride, float *lse, void *stream)
+{
+    if (!q || !k || !v || !idx || !slot_mask || !o) return fail(VEDA_ERR_NULL, "sparse_attn_fwd_tokens: NULL pointer");
+    if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "sparse_attn_fwd_tokens: d=%d unsupported", d);
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || (head_stride % 8) || (token_stride % 8) ||
+        (o_head_stride % 8) || (o_token_stride % 8) || head_stride == token_stride)
+        return fail(VEDA_ERR_ALIGN, "sparse_attn_fwd_tokens: pointers/strides must be 16-byte aligned and distinct");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    Shape sh;
+    HeadCfgs hc;
+    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    if (k_keep < 1 || k_keep > sh.NT)
+        return fail(VEDA_ERR_K_RANGE, "sparse_attn_fwd_tokens: k=%d outside [1, %d]", k_keep, sh.NT);
+    const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)d);
+    return launch_sparse_attn_tok(q, k, v, head_stride, token_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w,
+                                  sh.B, sh.NT, d, idx, slot_mask, k_keep, scale, o, o_head_stride, o_token_stride, lse,
+                                  S(stream));
 }
 
 veda_status veda_target_scores(const uint16_t *q_tiled, const uint16_t *k_tiled, const uint32_t *slot_mask,

@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -48,6 +49,65 @@ struct Params {
     float scale_log2;
     unsigned long long *trace;  // VEDA_ATTN_TRACE builds only: per-step clock64 stamps of CTA 0
 };
+
+// Token-layout mode (TOK): Q/K/V tiles are TMA'd straight from the token tensors with one
+// 5-D box per tile (make_tmap_tile_tokens: same smem image as the tiled copy, padded
+// slots zero-filled) and O rows are stored straight to token order, so the path needs no
+// tiled copies of Q, K, V or O.  Heads of one launch may use at
+// most MAXC distinct tile shapes (the host splits larger head sets into several launches).
+constexpr int MAXC = 8;
+struct TokParams {
+    CUtensorMap q[MAXC], k[MAXC], v[MAXC];
+    int T, H, W, Hp, Wp;
+    int tok_major;  // 1: coordinates (d, h, w, h', t); 0: (d, w, h', t, h)
+    int64_t o_hs, o_ts;
+    uint8_t pt[MAXC], ph[MAXC], pw[MAXC];
+    // per shape: tiles per padded row (nbw = Wp/pw) and per padded frame (nbhw), with
+    // ceil(2^32/n) multipliers: the single producer thread decodes a tile index per load,
+    // so the decode must not cost integer divisions
+    uint32_t nbw[MAXC], nbhw[MAXC], mbw[MAXC], mbhw[MAXC];
+    uint8_t cid[kMaxHeads];
+};
+
+// q = i / n, r = i % n for 0 <= i < 2^24 by a multiply-high with m = ceil(2^32 / n) and one correction
+__device__ __forceinline__ int div_magic(int i, uint32_t n, uint32_t m, int &r)
+{
+    int q = (int)__umulhi((uint32_t)i, m);
+    r = i - q * (int)n;
+    if (r < 0) { --q; r += (int)n; }
+    if (r >= (int)n) { ++q; r -= (int)n; }
+    return q;
+}
+
+struct TileOrigin {
+    int c, t0, h0, w0;
+};
+__device__ __forceinline__ TileOrigin tile_origin(const TokParams &tp, int h, int i)
+{
+    TileOrigin o;
+    o.c = tp.cid[h];
+    int rem, iw;
+    const int it = div_magic(i, tp.nbhw[o.c], tp.mbhw[o.c], rem);
+    const int ih = div_magic(rem, tp.nbw[o.c], tp.mbw[o.c], iw);
+    o.t0 = it * tp.pt[o.c];
+    o.h0 = ih * tp.ph[o.c];
+    o.w0 = iw * tp.pw[o.c];
+    return o;
+}
+// TMA of the NCH 64-channel chunks of tile (h, i) in token layout (chunk c lands at dst + c*stride)
+template <int NCH>
+__device__ __forceinline__ void tma_tile_tok(uint32_t dst, uint32_t stride, const CUtensorMap *maps,
+                                             const TokParams &tp, int h, int i, uint32_t bar)
+{
+    const TileOrigin o = tile_origin(tp, h, i);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        if (tp.tok_major)
+            tma_load_5d(dst + c * stride, &maps[o.c], c * 64, h, o.w0, o.h0, o.t0, bar);
+        else
+            tma_load_5d(dst + c * stride, &maps[o.c], c * 64, o.w0, o.h0, o.t0, h, bar);
+    }
+}
 
 #ifdef VEDA_ATTN_TRACE
 #define TR(role, step, field)                                                                      \
@@ -100,25 +160,23 @@ __device__ __forceinline__ void ex2_emu2(float &y0, float &y1, float x0, float x
 {
     x0 = fmaxf(x0, -125.0f);  // 2^n * p must stay a normal number (p in [0.7, 1.42))
     x1 = fmaxf(x1, -125.0f);
-    float j0, j1, t0, t1, f0, f1, p0, p1;
+    float j0, j1, p0, p1;
     asm("{\n\t.reg .b64 rx, rm, rj, rt, rf, rp, c3, c2, c1, c0;\n\t"
-        "mov.b64 rx, {%8, %9};\n\t"
-        "mov.b64 rm, {%10, %10};\n\t"
+        "mov.b64 rx, {%4, %5};\n\t"
+        "mov.b64 rm, {%6, %6};\n\t"
         "add.rn.f32x2 rj, rx, rm;\n\t"
         "sub.rn.f32x2 rt, rj, rm;\n\t"
         "sub.rn.f32x2 rf, rx, rt;\n\t"
-        "mov.b64 c3, {%11, %11};\n\t"
-        "mov.b64 c2, {%12, %12};\n\t"
-        "mov.b64 c1, {%13, %13};\n\t"
-        "mov.b64 c0, {%14, %14};\n\t"
+        "mov.b64 c3, {%7, %7};\n\t"
+        "mov.b64 c2, {%8, %8};\n\t"
+        "mov.b64 c1, {%9, %9};\n\t"
+        "mov.b64 c0, {%10, %10};\n\t"
         "fma.rn.f32x2 rp, rf, c3, c2;\n\t"
         "fma.rn.f32x2 rp, rp, rf, c1;\n\t"
         "fma.rn.f32x2 rp, rp, rf, c0;\n\t"
         "mov.b64 {%0, %1}, rj;\n\t"
-        "mov.b64 {%2, %3}, rt;\n\t"
-        "mov.b64 {%4, %5}, rf;\n\t"
-        "mov.b64 {%6, %7}, rp;\n\t}"
-        : "=f"(j0), "=f"(j1), "=f"(t0), "=f"(t1), "=f"(f0), "=f"(f1), "=f"(p0), "=f"(p1)
+        "mov.b64 {%2, %3}, rp;\n\t}"
+        : "=f"(j0), "=f"(j1), "=f"(p0), "=f"(p1)
         : "f"(x0), "f"(x1), "f"(12582912.0f), "f"(0.05517162f), "f"(0.24261113f), "f"(0.69326097f),
           "f"(0.99992806f));
     y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(j0) << 23));
@@ -152,11 +210,12 @@ __device__ __forceinline__ void fadd2_acc(float &s0, float &s1, float a, float b
 __device__ __forceinline__ float u2f(uint32_t u) { return __uint_as_float(u); }
 __device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
 
-template <int B, int D>
+template <int B, int D, bool TOK>
 __global__ void __launch_bounds__(NTHREADS, 1)
     sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                            const __grid_constant__ CUtensorMap tmK,
-                           const __grid_constant__ CUtensorMap tmV, const Params p)
+                           const __grid_constant__ CUtensorMap tmV, const Params p,
+                           const __grid_constant__ TokParams tp)
 {
     using G = Geo<B, D>;
     extern __shared__ uint8_t smem_raw[];
@@ -243,8 +302,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     qe_bits ^= 1u << s;
                     mbar_expect_tx(Q_FULL(s), B * D * 2);
 #pragma unroll
-                    for (int c = 0; c < D / 64; ++c)
-                        tma_load_2d(sQ + s * G::Q_BYTES + c * G::QCHUNK, &tmQ, c * 64, u[s] * B, Q_FULL(s));
+                    if (TOK)
+                        tma_tile_tok<D / 64>(sQ + s * G::Q_BYTES, G::QCHUNK, tp.q, tp, hh[s], u[s] - hh[s] * NT,
+                                             Q_FULL(s));
+                    else
+                        for (int c = 0; c < D / 64; ++c)
+                            tma_load_2d(sQ + s * G::Q_BYTES + c * G::QCHUNK, &tmQ, c * 64, u[s] * B, Q_FULL(s));
                 }
                 auto load_tile = [&](const CUtensorMap *tm, int h, int j) {
                     mbar_wait(RING_EMPTY(stage), ph ^ 1);
@@ -257,10 +320,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #endif
                     mbar_expect_tx(RING_FULL(stage), G::TILE_BYTES);
                     const int row = (h * NT + j) * B;
+                    if (TOK)
+                        tma_tile_tok<D / 64>(sRing + stage * G::TILE_BYTES, G::KCHUNK, tm == &tmK ? tp.k : tp.v, tp,
+                                             h, j, RING_FULL(stage));
+                    else
 #pragma unroll
-                    for (int c = 0; c < D / 64; ++c)
-                        tma_load_2d(sRing + stage * G::TILE_BYTES + c * G::KCHUNK, tm, c * 64, row,
-                                    RING_FULL(stage));
+                        for (int c = 0; c < D / 64; ++c)
+                            tma_load_2d(sRing + stage * G::TILE_BYTES + c * G::KCHUNK, tm, c * 64, row,
+                                        RING_FULL(stage));
                     if (++stage == G::NST) { stage = 0; ph ^= 1; }
                 };
 #pragma unroll
@@ -526,13 +593,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (row < B) qvalid = (__ldg(p.slot_mask + (size_t)u * G::MW + (row >> 5)) >> (row & 31)) & 1u;
             const float inv = (qvalid && l > 0.f) ? 1.f / l : 0.f;
             uint16_t *orow = p.out + ((size_t)u * B + (row < B ? row : 0)) * D;
+            bool store = row < B;
+            if (TOK) {  // row -> its token (reading R3); padded query slots have none
+                const TileOrigin o = tile_origin(tp, h, u - h * NT);
+                const int lpw = __ffs(tp.pw[o.c]) - 1, lphw = lpw + __ffs(tp.ph[o.c]) - 1;
+                const int t = o.t0 + (row >> lphw), hq = o.h0 + ((row >> lpw) & (tp.ph[o.c] - 1)),
+                          w = o.w0 + (row & (tp.pw[o.c] - 1));
+                store = store && qvalid;
+                orow = p.out + (size_t)h * tp.o_hs + (((size_t)t * tp.H + hq) * tp.W + w) * tp.o_ts;
+            }
 #pragma unroll
             for (int c = 0; c < D / 32; ++c) {
                 uint32_t o[32];
                 tmem_ld32(tO + c * 32, o);
                 tmem_wait_ld();
                 reg_fence(o);
-                if (row < B) {
+                if (store) {
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(u2f(o[2 * i]) * inv, u2f(o[2 * i + 1]) * inv);
@@ -556,25 +632,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 static unsigned long long *g_attn_trace = nullptr;
 
-template <int B, int D>
-static veda_status launch(const uint16_t *q, const uint16_t *k, const uint16_t *v, const int32_t *idx,
-                          const uint32_t *mask, int Hh, int NT, int kk, float scale, uint16_t *o,
-                          float *lse, cudaStream_t stream)
+template <int B, int D, bool TOK>
+static veda_status launch_kernel(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, const Params &p,
+                                 const TokParams &tp, int units, cudaStream_t stream)
 {
     using G = Geo<B, D>;
-    CUtensorMap mq, mk, mv;
-    const uint64_t rows = (uint64_t)Hh * NT * B;
-    veda_status st;
-    if ((st = make_tmap_bf16(&mq, q, rows, D, B)) != VEDA_OK) return st;
-    if ((st = make_tmap_bf16(&mk, k, rows, D, B)) != VEDA_OK) return st;
-    if ((st = make_tmap_bf16(&mv, v, rows, D, B)) != VEDA_OK) return st;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(sparse_attn_fwd_kernel<B, D>,
+        cudaError_t e = cudaFuncSetAttribute(sparse_attn_fwd_kernel<B, D, TOK>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
         if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
         attr_set = true;
     }
+    int grid = (units + NSLOT - 1) / NSLOT;
+    const int nsm = num_sms();
+    if (grid > nsm) grid = nsm;
+    sparse_attn_fwd_kernel<B, D, TOK><<<grid, NTHREADS, G::SMEM, stream>>>(mq, mk, mv, p, tp);
+    count_launch();
+    return check_launch("sparse_attn_fwd");
+}
+
+static Params make_params(const int32_t *idx, const uint32_t *mask, uint16_t *o, float *lse, int Hh, int NT, int kk,
+                          float scale)
+{
     Params p;
     p.idx = idx;
     p.slot_mask = mask;
@@ -585,13 +665,81 @@ static veda_status launch(const uint16_t *q, const uint16_t *k, const uint16_t *
     p.total_units = Hh * NT;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.trace = g_attn_trace;
-    const int units = Hh * NT;
-    int grid = (units + NSLOT - 1) / NSLOT;
-    const int nsm = num_sms();
-    if (grid > nsm) grid = nsm;
-    sparse_attn_fwd_kernel<B, D><<<grid, NTHREADS, G::SMEM, stream>>>(mq, mk, mv, p);
-    count_launch();
-    return check_launch("sparse_attn_fwd");
+    return p;
+}
+
+template <int B, int D>
+static veda_status launch(const uint16_t *q, const uint16_t *k, const uint16_t *v, const int32_t *idx,
+                          const uint32_t *mask, int Hh, int NT, int kk, float scale, uint16_t *o,
+                          float *lse, cudaStream_t stream)
+{
+    CUtensorMap mq, mk, mv;
+    const uint64_t rows = (uint64_t)Hh * NT * B;
+    veda_status st;
+    if ((st = make_tmap_bf16(&mq, q, rows, D, B)) != VEDA_OK) return st;
+    if ((st = make_tmap_bf16(&mk, k, rows, D, B)) != VEDA_OK) return st;
+    if ((st = make_tmap_bf16(&mv, v, rows, D, B)) != VEDA_OK) return st;
+    static TokParams tp_unused;  // zero-initialised; the tiled instantiation never reads it
+    return launch_kernel<B, D, false>(mq, mk, mv, make_params(idx, mask, o, lse, Hh, NT, kk, scale), tp_unused,
+                                      Hh * NT, stream);
+}
+
+// Token-layout launch: heads are split into consecutive groups with at most MAXC distinct
+// tile shapes; each group is one launch on pointers offset to its first head.
+template <int B, int D>
+static veda_status launch_tok(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t hs, int64_t ts,
+                              const HeadCfgs &cf, int Hh, int Hp, int Wp, int T, int H, int W, int NT,
+                              const int32_t *idx, const uint32_t *mask, int kk, float scale, uint16_t *o,
+                              int64_t o_hs, int64_t o_ts, float *lse, cudaStream_t stream)
+{
+    static TokParams tp;  // host staging (3-4 KB): filled per launch, passed by value
+    CUtensorMap dummy;
+    memset(&dummy, 0, sizeof dummy);
+    const int MW = B / 32;
+    for (int h0 = 0; h0 < Hh;) {
+        int nc = 0, h1 = h0;
+        for (; h1 < Hh; ++h1) {
+            int c = 0;
+            while (c < nc && !(tp.pt[c] == cf.pt[h1] && tp.ph[c] == cf.ph[h1] && tp.pw[c] == cf.pw[h1])) ++c;
+            if (c == nc) {
+                if (nc == MAXC) break;
+                tp.pt[c] = cf.pt[h1]; tp.ph[c] = cf.ph[h1]; tp.pw[c] = cf.pw[h1];
+                ++nc;
+            }
+            tp.cid[h1 - h0] = (uint8_t)c;
+        }
+        const int hn = h1 - h0;
+        veda_status st;
+        int tm = 0;
+        for (int c = 0; c < nc; ++c) {
+            if ((st = make_tmap_tile_tokens(&tp.q[c], q + (size_t)h0 * hs, hs, ts, hn, T, H, W, D, tp.pt[c], tp.ph[c],
+                                            tp.pw[c], &tm)) != VEDA_OK ||
+                (st = make_tmap_tile_tokens(&tp.k[c], k + (size_t)h0 * hs, hs, ts, hn, T, H, W, D, tp.pt[c], tp.ph[c],
+                                            tp.pw[c], &tm)) != VEDA_OK ||
+                (st = make_tmap_tile_tokens(&tp.v[c], v + (size_t)h0 * hs, hs, ts, hn, T, H, W, D, tp.pt[c], tp.ph[c],
+                                            tp.pw[c], &tm)) != VEDA_OK)
+                return st;
+        }
+        for (int c = 0; c < nc; ++c) {
+            tp.nbw[c] = (uint32_t)(Wp / tp.pw[c]);
+            tp.nbhw[c] = (uint32_t)((Hp / tp.ph[c]) * (Wp / tp.pw[c]));
+            auto magic = [](uint32_t n) {  // ceil(2^32 / n), saturated for n = 1 (div_magic corrects by one)
+                const unsigned long long m = (0x100000000ull + n - 1) / n;
+                return (uint32_t)(m > 0xFFFFFFFFull ? 0xFFFFFFFFull : m);
+            };
+            tp.mbw[c] = magic(tp.nbw[c]);
+            tp.mbhw[c] = magic(tp.nbhw[c]);
+        }
+        tp.T = T; tp.H = H; tp.W = W; tp.Hp = Hp; tp.Wp = Wp;
+        tp.tok_major = tm;
+        tp.o_hs = o_hs;
+        tp.o_ts = o_ts;
+        const Params p = make_params(idx + (size_t)h0 * NT * kk, mask + (size_t)h0 * NT * MW, o + (size_t)h0 * o_hs,
+                                     lse ? lse + (size_t)h0 * NT * B : nullptr, hn, NT, kk, scale);
+        if ((st = launch_kernel<B, D, true>(dummy, dummy, dummy, p, tp, hn * NT, stream)) != VEDA_OK) return st;
+        h0 = h1;
+    }
+    return VEDA_OK;
 }
 
 }  // namespace attn
@@ -617,6 +765,21 @@ veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint1
     if (B == 64 && d == 128) return attn::launch<64, 128>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
     if (B == 64 && d == 64) return attn::launch<64, 64>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
     return fail(VEDA_ERR_CONFIG, "sparse_attn_fwd: unsupported (B=%d, d=%d)", B, d);
+}
+
+veda_status launch_sparse_attn_tok(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t hs, int64_t ts,
+                                   const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp, int T, int H, int W, int B,
+                                   int NT, int d, const int32_t *idx, const uint32_t *mask, int kk, float scale,
+                                   uint16_t *o, int64_t o_hs, int64_t o_ts, float *lse, cudaStream_t s)
+{
+    (void)Tp;
+#define VEDA_TOK_ARGS q, k, v, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, idx, mask, kk, scale, o, o_hs, o_ts, lse, s
+    if (B == 128 && d == 128) return attn::launch_tok<128, 128>(VEDA_TOK_ARGS);
+    if (B == 128 && d == 64) return attn::launch_tok<128, 64>(VEDA_TOK_ARGS);
+    if (B == 64 && d == 128) return attn::launch_tok<64, 128>(VEDA_TOK_ARGS);
+    if (B == 64 && d == 64) return attn::launch_tok<64, 64>(VEDA_TOK_ARGS);
+#undef VEDA_TOK_ARGS
+    return fail(VEDA_ERR_CONFIG, "sparse_attn_fwd_tokens: unsupported (B=%d, d=%d)", B, d);
 }
 
 }  // namespace veda

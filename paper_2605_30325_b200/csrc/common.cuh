@@ -21,6 +21,15 @@ int num_sms();
 veda_status make_tmap_bf16(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols,
                            uint32_t box_rows);
 
+// 5-D bf16 tensor map over a token tensor x[h][n][c] (element strides head_stride,
+// token_stride; n = (t*H + h')*W + w) whose box is ONE tile of shape (pt, ph, pw) x 64
+// channels: the box lands in smem as pt*ph*pw rows of 128 B in slot order (reading R3),
+// SWIZZLE_128B, out-of-grid slots zero-filled (reading R4) -- the same image as a 2-D box
+// of the tiled tensor.  Dimension order follows the strides (head-major: d,W,H,T,Hh;
+// token-major: d,Hh,W,H,T); *tok_major reports which.
+veda_status make_tmap_tile_tokens(CUtensorMap *map, const void *base, int64_t head_stride, int64_t token_stride,
+                                  int Hh, int T, int H, int W, int d, int pt, int ph, int pw, int *tok_major);
+
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 constexpr int kMaxHeads = 1024;
@@ -56,6 +65,14 @@ veda_status launch_topk(const float *scores, int Hh, int NT, int k, int32_t *idx
 veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v,
                                const int32_t *idx, const uint32_t *mask, int Hh, int NT, int B, int d,
                                int kk, float scale, uint16_t *o, float *lse, cudaStream_t s);
+// attention straight from / to the token layout (no tiled copies)
+veda_status launch_sparse_attn_tok(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t hs, int64_t ts,
+                                   const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp, int T, int H, int W, int B,
+                                   int NT, int d, const int32_t *idx, const uint32_t *mask, int kk, float scale,
+                                   uint16_t *o, int64_t o_hs, int64_t o_ts, float *lse, cudaStream_t s);
+veda_status launch_tile_pool_tokens(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfgs &cf, int Hh, int Tp,
+                                    int Hp, int Wp, int T, int H, int W, int B, int NT, int d, float *z,
+                                    int32_t *cnt, uint32_t *mask, cudaStream_t s);
 veda_status launch_sparse_attn_1q(const uint16_t *q, const uint16_t *k, const uint16_t *v, const int32_t *idx,
                                   const uint32_t *mask, int Hh, int NT, int B, int d, int kk, float scale,
                                   uint16_t *o, float *lse, cudaStream_t s);

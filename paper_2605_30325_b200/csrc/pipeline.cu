@@ -5,16 +5,19 @@
 // PAPER.md:693-698), so the call is cut into chunks of heads and software-pipelined over
 // three streams and two device buffer sets ("slots"):
 //
-//   h2d stream     : copy Q/K/V of chunk c            (waits: permutes of chunk c-2 done)
-//   caller stream  : permute x3 -> score -> top-k -> attention -> unpermute of chunk c
+//   h2d stream     : copy Q/K/V of chunk c            (waits: attention of chunk c-2 done)
+//   caller stream  : pool Q/K -> score -> top-k -> attention (token layout in and out)
 //                                                     (waits: H2D of c, D2H of chunk c-2)
 //   d2h stream     : copy O of chunk c back to host   (waits: compute of c)
 //
-// so the PCIe transfers in both directions overlap the kernels.  Every chunk is tiled on
-// the padded grid of the WHOLE call (reading R5), so results are bit-identical to one
-// call over all heads.  Pure host code: only the existing kernels run.
+// so the PCIe transfers in both directions overlap the kernels.  The chunk runs the
+// token-layout form of the path (veda_tile_pool, veda_tile_score_pooled, veda_select_topk,
+// veda_sparse_attn_fwd_tokens): no tiled copies.  Every chunk is tiled on the padded grid
+// of the WHOLE call (reading R5), so results are bit-identical to one call over all heads.
+// Pure host code: only the existing kernels run.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <mutex>
 #include <vector>
 
@@ -55,7 +58,7 @@ int chunk_heads(int Hh, int heads_per_chunk)
 
 // byte offsets of one slot's buffers
 struct SlotLayout {
-    size_t in, tiled, out, cnt, mask, scores, idx, ws, ws_bytes, total;
+    size_t in, out, z, cnt, mask, scores, idx, ws, ws_bytes, total;
 };
 
 veda_status slot_layout(int hc, int64_t N, const Shape &sh, int d, int k, const veda_scorer *w, SlotLayout *L)
@@ -64,11 +67,10 @@ veda_status slot_layout(int hc, int64_t N, const Shape &sh, int d, int k, const 
     veda_status st = veda_tile_score_workspace(hc, sh.NT, d, w, &ws);
     if (st != VEDA_OK) return st;
     const size_t tok = align256((size_t)hc * N * d * 2);
-    const size_t til = align256((size_t)hc * sh.NT * sh.B * d * 2);
     size_t p = 0;
     L->in = p; p += 3 * tok;
-    L->tiled = p; p += 4 * til;
     L->out = p; p += tok;
+    L->z = p; p += 2 * align256((size_t)hc * sh.NT * 3 * d * 4);
     L->cnt = p; p += align256((size_t)hc * sh.NT * 4);
     L->mask = p; p += align256((size_t)hc * sh.NT * (sh.B / 32) * 4);
     L->scores = p; p += align256((size_t)hc * sh.NT * sh.NT * 4);
@@ -171,16 +173,16 @@ veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k
     VEDA_CU(cudaStreamWaitEvent(side.d2h, ev_start, 0));
 
     const size_t tok = align256((size_t)hc * N * d * 2);
-    const size_t til = align256((size_t)hc * sh.NT * sh.B * d * 2);
+    const size_t zb = align256((size_t)hc * sh.NT * 3 * d * 4);
     const uint16_t *src[3] = {q_host, k_host, v_host};
     for (int c = 0; c < n_chunks; ++c) {
         const int h0 = c * hc;
         const int hn = (h0 + hc <= Hh) ? hc : Hh - h0;
         char *slot = static_cast<char *>(workspace) + (size_t)(c % kSlots) * L.total;
-        uint16_t *in[3], *tl[4];
+        uint16_t *in[3];
         for (int j = 0; j < 3; ++j) in[j] = reinterpret_cast<uint16_t *>(slot + L.in + j * tok);
-        for (int j = 0; j < 4; ++j) tl[j] = reinterpret_cast<uint16_t *>(slot + L.tiled + j * til);
         uint16_t *out = reinterpret_cast<uint16_t *>(slot + L.out);
+        float *zq = reinterpret_cast<float *>(slot + L.z), *zk = reinterpret_cast<float *>(slot + L.z + zb);
         int32_t *cnt = reinterpret_cast<int32_t *>(slot + L.cnt);
         uint32_t *mask = reinterpret_cast<uint32_t *>(slot + L.mask);
         float *scores = reinterpret_cast<float *>(slot + L.scores);
@@ -190,7 +192,7 @@ veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k
         const int64_t dhs = head_major ? N * d : d;
         const int64_t dts = head_major ? d : (int64_t)hn * d;
 
-        // 1. H2D of chunk c into slot c % 2 once chunk c-2 has been tiled
+        // 1. H2D of chunk c into slot c % 2 once the attention of chunk c-2 has read it
         if (c >= kSlots) VEDA_CU(cudaStreamWaitEvent(side.h2d, ev_infree[c - kSlots], 0));
         for (int j = 0; j < 3; ++j) {
             if (head_major)
@@ -202,33 +204,29 @@ veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k
         }
         VEDA_CU(cudaEventRecord(ev_h2d[c], side.h2d));
 
-        // 2. the five steps on the caller's stream
+        // 2. the path on the caller's stream (token layout in and out)
         VEDA_CU(cudaStreamWaitEvent(cs, ev_h2d[c], 0));
         HeadCfgs hcf;
         for (int h = 0; h < hn; ++h) { hcf.pt[h] = all.pt[h0 + h]; hcf.ph[h] = all.ph[h0 + h]; hcf.pw[h] = all.pw[h0 + h]; }
-        if ((st = launch_tile_permute(in[0], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B, sh.NT,
-                                      d, tl[0], cnt, mask, nullptr, cs)) != VEDA_OK)
+        if ((st = launch_tile_pool_tokens(in[0], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
+                                          sh.NT, d, zq, cnt, mask, cs)) != VEDA_OK ||
+            (st = launch_tile_pool_tokens(in[1], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
+                                          sh.NT, d, zk, nullptr, nullptr, cs)) != VEDA_OK)
             return st;
-        for (int j = 1; j < 3; ++j)
-            if ((st = launch_tile_permute(in[j], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
-                                          sh.NT, d, tl[j], nullptr, nullptr, nullptr, cs)) != VEDA_OK)
-                return st;
-        VEDA_CU(cudaEventRecord(ev_infree[c], cs));
         veda_scorer wc = *w;
         const size_t o1 = (size_t)h0 * w->d_in * w->d_hidden, o2 = (size_t)h0 * w->d_hidden * w->d_lat;
         wc.w1q += o1; wc.w1k += o1; wc.b1q += (size_t)h0 * w->d_hidden; wc.b1k += (size_t)h0 * w->d_hidden;
         wc.w2q += o2; wc.w2k += o2; wc.b2q += (size_t)h0 * w->d_lat; wc.b2k += (size_t)h0 * w->d_lat;
-        if ((st = veda_tile_score(tl[0], tl[1], cnt, mask, hn, sh.NT, sh.B, d, &wc, scores, ws, L.ws_bytes, cs)) !=
-            VEDA_OK)
+        if ((st = veda_tile_score_pooled(zq, zk, cnt, hn, sh.NT, d, &wc, scores, ws, L.ws_bytes, cs)) != VEDA_OK)
             return st;
         if ((st = veda_select_topk(scores, hn, sh.NT, k, idx, cs)) != VEDA_OK) return st;
-        if ((st = veda_sparse_attn_fwd(tl[0], tl[1], tl[2], idx, mask, hn, sh.NT, sh.B, d, k, 0.f, tl[3], nullptr,
-                                       cs)) != VEDA_OK)
-            return st;
         if (c >= kSlots) VEDA_CU(cudaStreamWaitEvent(cs, ev_d2h[c - kSlots], 0));  // out slot drained
-        if ((st = launch_tile_unpermute(tl[3], hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B, sh.NT, d, out,
-                                        dhs, dts, cs)) != VEDA_OK)
+        const float scale = 1.0f / std::sqrt((float)d);
+        if ((st = launch_sparse_attn_tok(in[0], in[1], in[2], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h,
+                                         lat.w, sh.B, sh.NT, d, idx, mask, k, scale, out, dhs, dts, nullptr, cs)) !=
+            VEDA_OK)
             return st;
+        VEDA_CU(cudaEventRecord(ev_infree[c], cs));  // the attention was the last reader of Q/K/V
         VEDA_CU(cudaEventRecord(ev_comp[c], cs));
 
         // 3. D2H of chunk c

@@ -29,7 +29,8 @@ EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_worksp
            "veda_trippool", "veda_project", "veda_pair_scores", "veda_status_str", "veda_last_error",
            "veda_launch_count", "veda_check_device", "veda_tile_permute_pool", "veda_tile_score_pooled",
            "veda_target_scores", "veda_tile_recall", "veda_tile_permute_scalar", "veda_tile_unpermute_scalar",
-           "veda_sq_err", "veda_sparse_attention_host_workspace", "veda_sparse_attention_host"]
+           "veda_sq_err", "veda_sparse_attention_host_workspace", "veda_sparse_attention_host",
+           "veda_tile_pool", "veda_sparse_attn_fwd_tokens"]
 
 
 class VedaError(RuntimeError):
@@ -88,6 +89,9 @@ def load(path: str = LIB_PATH):
         "veda_sq_err": ([P, P, i64, i64, i32, P, P], i32),
         "veda_sparse_attention_host_workspace": ([Latent, P, i32, i32, i32, P, i32, P], i32),
         "veda_sparse_attention_host": ([P, P, P, i64, i64, Latent, P, i32, i32, i32, P, i32, P, P, sz, P], i32),
+        "veda_tile_pool": ([P, i64, i64, Latent, P, i32, i32, P, P, P, P], i32),
+        "veda_sparse_attn_fwd_tokens": ([P, P, P, i64, i64, Latent, P, i32, i32, P, P, i32, f32, P, i64, i64, P, P],
+                                        i32),
         "veda_status_str": ([i32], ctypes.c_char_p),
         "veda_last_error": ([], ctypes.c_char_p),
         "veda_launch_count": ([], ctypes.c_uint64),
@@ -350,6 +354,44 @@ def sparse_attn_fwd(q_tiled, k_tiled, v_tiled, idx, slot_mask, scale: float = 0.
     return (out, lse) if want_lse else out
 
 
+def tile_pool(x: torch.Tensor, lat, cfgs, z=None, meta=True):
+    """TripPool of every tile of x [Hh, N, d] read straight from token order (veda_tile_pool).
+    Returns (z [Hh, N_T, 3d] fp32, tile_count | None, slot_mask | None)."""
+    _need_cuda(x)
+    assert x.dtype == torch.bfloat16 and x.dim() == 3 and x.stride(2) == 1
+    Hh, N, d = x.shape
+    sh = tiled_shape(lat, cfgs, Hh)
+    if z is None:
+        z = torch.empty((Hh, sh.n_tiles, 3 * d), dtype=torch.float32, device=x.device)
+    cnt = mask = None
+    if meta:
+        cnt = torch.empty((Hh, sh.n_tiles), dtype=torch.int32, device=x.device)
+        mask = torch.empty((Hh, sh.n_tiles, sh.B // 32), dtype=torch.int32, device=x.device)
+    _check(load().veda_tile_pool(_ptr(x), x.stride(0), x.stride(1), Latent(*lat), _cfg_array(cfgs, Hh), Hh, d,
+                                 _ptr(z), _ptr(cnt), _ptr(mask), _stream()), "tile_pool")
+    return z, cnt, mask
+
+
+def sparse_attn_fwd_tokens(q, k, v, lat, cfgs, idx, slot_mask, scale: float = 0.0, out=None, want_lse=False):
+    """Attention + untiling straight on token tensors [Hh, N, d] (veda_sparse_attn_fwd_tokens).
+    Rows of padded slots are not written, so ``out`` (default: zeros) keeps its values there."""
+    _need_cuda(q, k, v, idx, slot_mask)
+    Hh, N, d = q.shape
+    if not (k.stride() == q.stride() and v.stride() == q.stride()):
+        raise VedaError("sparse_attn_fwd_tokens: q, k, v must share strides")
+    NT, kk = idx.shape[1], idx.shape[2]
+    B = slot_mask.shape[2] * 32
+    if out is None:
+        out = torch.zeros((Hh, N, d), dtype=torch.bfloat16, device=q.device)
+    lse = torch.empty((Hh, NT, B), dtype=torch.float32, device=q.device) if want_lse else None
+    st = load().veda_sparse_attn_fwd_tokens(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), Latent(*lat),
+                                            _cfg_array(cfgs, Hh), Hh, d, _ptr(idx), _ptr(slot_mask), kk,
+                                            float(scale), _ptr(out), out.stride(0), out.stride(1), _ptr(lse),
+                                            _stream())
+    _check(st, "sparse_attn_fwd_tokens")
+    return (out, lse) if want_lse else out
+
+
 def target_scores(q_tiled, k_tiled, slot_mask, lse, scale: float = 0.0, out=None):
     """Eq. 4 pass 2: S_tgt [Hh, N_T, N_T] fp32 from the dense lse (see oracle_tile_mask)."""
     _need_cuda(q_tiled, k_tiled, slot_mask, lse)
@@ -390,25 +432,49 @@ def tile_recall(idx_sp, idx_fu, tile_count=None, n_tiles=None, out=None):
 class SparseAttention:
     """The whole hot path with preallocated buffers (one DiT attention layer call).
 
-    q, k, v: bf16 [Hh, N, d] views on the GPU.  Steps (Alg. 2 + Eq. 2):
-    permute Q/K/V -> tile_score -> select_topk -> sparse_attn_fwd -> unpermute.
+    q, k, v: bf16 [Hh, N, d] views on the GPU (any head / token strides shared by the
+    three).  Steps (Alg. 2 + Eq. 2):
+
+    * ``mode="tokens"`` (default): tile_pool Q/K (TripPool read
+      straight from token order) -> tile_score_pooled -> select_topk ->
+      sparse_attn_fwd_tokens (tiles TMA'd from token order, rows stored to token order);
+      no tiled copy of Q, K, V or O exists;
+    * ``mode="tiled"``: permute Q/K/V -> tile_score -> select_topk -> sparse_attn_fwd ->
+      unpermute (the five-call form of include/veda.h; bit-identical output).
     """
 
-    def __init__(self, lat, cfgs, Hh, d, scorer_weights: dict, sparsity=None, k=None, device="cuda"):
-        self.lat, self.cfgs, self.Hh, self.d = tuple(lat), list(cfgs), Hh, d
+    STEPS = {"tokens": ("pool", "score", "topk", "attn", "untile"),
+             "tiled": ("permute", "score", "topk", "attn", "unpermute")}
+
+    def __init__(self, lat, cfgs, Hh, d, scorer_weights: dict, sparsity=None, k=None, device="cuda",
+                 mode="tokens"):
+        if mode not in self.STEPS:
+            raise VedaError(f"mode must be one of {list(self.STEPS)}")
+        self.lat, self.cfgs, self.Hh, self.d, self.mode = tuple(lat), list(cfgs), Hh, d, mode
         self.shape = tiled_shape(lat, cfgs, Hh)
         NT, B = self.shape.n_tiles, self.shape.B
         self.k = k if k is not None else k_for_sparsity(NT, sparsity)
         self.weights = scorer_weights
         self.scorer = make_scorer(scorer_weights)
         dev = torch.device(device)
-        mk = lambda: torch.empty((Hh, NT, B, d), dtype=torch.bfloat16, device=dev)
-        self.qt, self.kt, self.vt, self.ot = mk(), mk(), mk(), mk()
+        self.device = dev
+        if mode == "tiled":
+            mk = lambda: torch.empty((Hh, NT, B, d), dtype=torch.bfloat16, device=dev)
+            self.qt, self.kt, self.vt, self.ot = mk(), mk(), mk(), mk()
+        else:
+            self.zq = torch.empty((Hh, NT, 3 * d), dtype=torch.float32, device=dev)
+            self.zk = torch.empty((Hh, NT, 3 * d), dtype=torch.float32, device=dev)
         self.cnt = torch.empty((Hh, NT), dtype=torch.int32, device=dev)
         self.mask = torch.empty((Hh, NT, B // 32), dtype=torch.int32, device=dev)
         self.scores = torch.empty((Hh, NT, NT), dtype=torch.float32, device=dev)
         self.idx = torch.empty((Hh, NT, self.k), dtype=torch.int32, device=dev)
         self.ws = ScoreWorkspace(Hh, NT, d, self.scorer, dev)
+
+    def tiled(self, q, k, v):
+        """Tiled copies (q~, k~, v~) of the inputs (for the oracle-mask / target tools)."""
+        lat, cfgs = self.lat, self.cfgs
+        return (tile_permute(q, lat, cfgs, meta=False)[0], tile_permute(k, lat, cfgs, meta=False)[0],
+                tile_permute(v, lat, cfgs, meta=False)[0])
 
     def __call__(self, q, k, v, out=None, events=None):
         """Run the path; ``events`` (optional list of 6 torch.cuda.Event) brackets the steps."""
@@ -417,10 +483,35 @@ class SparseAttention:
         cfg = _cfg_array(self.cfgs, Hh)
         NT, B = self.shape.n_tiles, self.shape.B
         if out is None:
-            out = torch.empty((Hh, self.lat[0] * self.lat[1] * self.lat[2], d), dtype=torch.bfloat16, device=q.device)
+            out = torch.zeros((Hh, self.lat[0] * self.lat[1] * self.lat[2], d), dtype=torch.bfloat16,
+                              device=q.device)
         ev = events or [None] * 6
-        if ev[0] is not None:
-            ev[0].record()
+
+        def mark(i):
+            if ev[i] is not None:
+                ev[i].record()
+
+        mark(0)
+        if self.mode == "tokens":
+            if not (k.stride() == q.stride() and v.stride() == q.stride()):
+                raise VedaError("q, k, v must share strides")
+            _check(lib.veda_tile_pool(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, _ptr(self.zq),
+                                      _ptr(self.cnt), _ptr(self.mask), s), "tile_pool(q)")
+            _check(lib.veda_tile_pool(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, _ptr(self.zk), None, None,
+                                      s), "tile_pool(k)")
+            mark(1)
+            _check(lib.veda_tile_score_pooled(_ptr(self.zq), _ptr(self.zk), _ptr(self.cnt), Hh, NT, d,
+                                              ctypes.byref(self.scorer), _ptr(self.scores), _ptr(self.ws.buf),
+                                              self.ws.nbytes, s), "tile_score_pooled")
+            mark(2)
+            _check(lib.veda_select_topk(_ptr(self.scores), Hh, NT, self.k, _ptr(self.idx), s), "select_topk")
+            mark(3)
+            _check(lib.veda_sparse_attn_fwd_tokens(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat, cfg,
+                                                   Hh, d, _ptr(self.idx), _ptr(self.mask), self.k, 0.0, _ptr(out),
+                                                   out.stride(0), out.stride(1), None, s), "sparse_attn_fwd_tokens")
+            mark(4)
+            mark(5)
+            return out
         # Q/K tiling and TripPool as two HBM-bound passes: measured faster than the fused
         # veda_tile_permute_pool (its extra registers halve the occupancy of the copy)
         _check(lib.veda_tile_permute(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, _ptr(self.qt),
@@ -429,27 +520,23 @@ class SparseAttention:
                                      s), "tile_permute(k)")
         _check(lib.veda_tile_permute(_ptr(v), v.stride(0), v.stride(1), lat, cfg, Hh, d, _ptr(self.vt), None, None,
                                      s), "tile_permute(v)")
-        if ev[1] is not None:
-            ev[1].record()
+        mark(1)
         _check(lib.veda_tile_score(_ptr(self.qt), _ptr(self.kt), _ptr(self.cnt), _ptr(self.mask), Hh, NT, B, d,
                                    ctypes.byref(self.scorer), _ptr(self.scores), _ptr(self.ws.buf), self.ws.nbytes, s),
                "tile_score")
-        if ev[2] is not None:
-            ev[2].record()
+        mark(2)
         _check(lib.veda_select_topk(_ptr(self.scores), Hh, NT, self.k, _ptr(self.idx), s), "select_topk")
-        if ev[3] is not None:
-            ev[3].record()
+        mark(3)
         _check(lib.veda_sparse_attn_fwd(_ptr(self.qt), _ptr(self.kt), _ptr(self.vt), _ptr(self.idx), _ptr(self.mask),
                                         Hh, NT, B, d, self.k, 0.0, _ptr(self.ot), None, s), "sparse_attn_fwd")
-        if ev[4] is not None:
-            ev[4].record()
+        mark(4)
         _check(lib.veda_tile_unpermute(_ptr(self.ot), lat, cfg, Hh, d, _ptr(out), out.stride(0), out.stride(1), s),
                "tile_unpermute")
-        if ev[5] is not None:
-            ev[5].record()
+        mark(5)
         return out
 
-    LAUNCHES_PER_CALL = 3 + 2 + 4 + 1 + 1 + 1 + 1  # permute x3, pool x2, mlp 2x2, scores, topk, attn, unpermute
+    # tokens: pool x2, mlp 2x2, scores, topk, attn;  tiled: permute x3, pool x2, mlp 2x2, scores, topk, attn, unpermute
+    LAUNCHES_PER_CALL = {"tokens": 2 + 4 + 1 + 1 + 1, "tiled": 3 + 2 + 4 + 1 + 1 + 1 + 1}
 
     def run_host(self, q, k, v, out=None, heads_per_chunk: int = 0):
         """The same call on HOST tensors (veda_sparse_attention_host): q, k, v, out are
@@ -475,7 +562,7 @@ class SparseAttention:
             _check(lib.veda_sparse_attention_host_workspace(lat, cfg, Hh, d, self.k, ctypes.byref(self.scorer),
                                                             heads_per_chunk, ctypes.byref(nb)),
                    "sparse_attention_host_workspace")
-            self._host_ws = torch.empty(nb.value, dtype=torch.uint8, device=self.qt.device)
+            self._host_ws = torch.empty(nb.value, dtype=torch.uint8, device=self.device)
             self._host_ws_key = key
         _check(lib.veda_sparse_attention_host(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat, cfg, Hh, d,
                                               self.k, ctypes.byref(self.scorer), heads_per_chunk, _ptr(out),

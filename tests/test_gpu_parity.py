@@ -287,26 +287,83 @@ def test_nhd_layout_strided_permute(V):
     assert torch.equal(out, q_nhd)
 
 
-def test_end_to_end_path_object(V, oracle):
-    """SparseAttention (the bench's launch configuration) equals the step-wise calls."""
+@pytest.mark.parametrize("mode", ["tokens", "tiled"])
+def test_end_to_end_path_object(V, oracle, mode):
+    """SparseAttention (the bench's launch configuration) equals the step-wise tiled calls."""
     c = Case("wan_slice", **CASES["wan_slice"])
     dev = torch.device("cuda")
     w = {n: t.to(dev) for n, t in c.w.items()}
-    path = V.SparseAttention(c.lat, c.cfgs, c.Hh, c.d, w, sparsity=c.sparsity)
+    path = V.SparseAttention(c.lat, c.cfgs, c.Hh, c.d, w, sparsity=c.sparsity, mode=mode)
     q, k, v = (t.to(dev) for t in (c.q, c.k, c.v))
     n0 = V.launch_count()
     o = path(q, k, v)
     torch.cuda.synchronize()
-    assert V.launch_count() - n0 == path.LAUNCHES_PER_CALL
+    assert V.launch_count() - n0 == path.LAUNCHES_PER_CALL[mode]
     qt, cnt, mask = V.tile_permute(q, c.lat, c.cfgs)
     kt, _, _ = V.tile_permute(k, c.lat, c.cfgs, meta=False)
     vt, _, _ = V.tile_permute(v, c.lat, c.cfgs, meta=False)
     s = V.tile_score(qt, kt, cnt, mask, V.make_scorer(w))
     idx = V.select_topk(s, path.k)
     o2 = V.tile_unpermute(V.sparse_attn_fwd(qt, kt, vt, idx, mask), c.lat, c.cfgs)
-    assert torch.equal(path.idx, idx) and torch.equal(o, o2)
+    assert torch.equal(path.idx, idx) and torch.equal(path.scores, s) and torch.equal(o, o2)
     # deterministic: a second call is bit-identical
     assert torch.equal(path(q, k, v), o)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_tile_pool_equals_permute_then_trippool(V, name):
+    """veda_tile_pool (TripPool read straight from token order) is bit-identical to
+    veda_tile_permute + veda_trippool, with the same tile counts and slot masks."""
+    c = Case(name, **CASES[name])
+    dev = torch.device("cuda")
+    for layout in ("hnd", "nhd"):
+        x = c.q.to(dev) if layout == "hnd" else c.q.transpose(0, 1).contiguous().to(dev).transpose(0, 1)
+        xt, cnt, mask = V.tile_permute(x, c.lat, c.cfgs)
+        z, cnt2, mask2 = V.tile_pool(x, c.lat, c.cfgs)
+        assert torch.equal(z.view(torch.int32), V.trippool(xt, mask).view(torch.int32))
+        assert torch.equal(cnt, cnt2) and torch.equal(mask, mask2)
+
+
+def _many_cfg_case(B, Hh):
+    """Heads cycling through every ordered (p_t, p_h, p_w) of power-of-two extents with
+    product B: more than 8 distinct shapes, so the token-layout attention splits the call
+    into several launches."""
+    shapes = [(a, b, B // (a * b)) for a in (1, 2, 4, 8, 16) for b in (1, 2, 4, 8, 16)
+              if B % (a * b) == 0 and B // (a * b) <= 16]
+    return [shapes[(3 * h) % len(shapes)] for h in range(Hh)]
+
+
+@pytest.mark.parametrize("name", list(CASES) + ["many_cfgs"])
+def test_attention_tokens_equals_tiled(V, name):
+    """veda_sparse_attn_fwd_tokens (tiles TMA'd from token order, rows stored to token
+    order) == veda_tile_permute x3 -> veda_sparse_attn_fwd -> veda_tile_unpermute, bit for
+    bit, for both token layouts; padded slots are never written; lse identical."""
+    if name == "many_cfgs":
+        c = Case("mixed_cfgs", lat=(9, 10, 13), cfgs=_many_cfg_case(64, 12), d=64, Hh=12, k=7)
+    else:
+        c = Case(name, **CASES[name])
+    dev = torch.device("cuda")
+    q, k, v = (t.to(dev) for t in (c.q, c.k, c.v))
+    qt, cnt, mask = V.tile_permute(q, c.lat, c.cfgs)
+    kt, _, _ = V.tile_permute(k, c.lat, c.cfgs, meta=False)
+    vt, _, _ = V.tile_permute(v, c.lat, c.cfgs, meta=False)
+    NT = qt.shape[1]
+    kk = c.k_keep if c.k_keep is not None else V.k_for_sparsity(NT, c.sparsity)
+    from paper_2605_30325_b200 import synth
+    idx = synth.random_index_lists(c.Hh, NT, kk, seed_parts=("tok", name)).to(dev)
+    ot, lse = V.sparse_attn_fwd(qt, kt, vt, idx, mask, want_lse=True)
+    want = V.tile_unpermute(ot, c.lat, c.cfgs)
+    for layout in ("hnd", "nhd"):
+        if layout == "hnd":
+            qq, kq, vq = q, k, v
+            out = torch.full_like(q, 7.0)
+        else:
+            qq, kq, vq = (t.transpose(0, 1).contiguous().transpose(0, 1) for t in (q, k, v))
+            out = torch.full_like(q.transpose(0, 1), 7.0).transpose(0, 1)
+        got, lse2 = V.sparse_attn_fwd_tokens(qq, kq, vq, c.lat, c.cfgs, idx, mask, out=out, want_lse=True)
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(torch.int16), want.view(torch.int16)), layout
+        assert torch.equal(lse, lse2)
 
 
 def test_waver_full_size_sampled(V, oracle):
@@ -330,8 +387,8 @@ def test_waver_full_size_sampled(V, oracle):
         oq, ocnt, omask = oracle.tile_permute(qh, pre.lat, [pre.cfg])
         ok_, _, _ = oracle.tile_permute(kh, pre.lat, [pre.cfg])
         ov, _, _ = oracle.tile_permute(vh, pre.lat, [pre.cfg])
-        assert np.array_equal(u16(path.qt[h:h + 1]), oq) and np.array_equal(u16(path.vt[h:h + 1]), ov)
         assert np.array_equal(bits32(path.mask[h:h + 1]), omask)
+        assert np.array_equal(path.cnt[h:h + 1].cpu().numpy(), ocnt)
         wn = {n: t[h:h + 1].cpu().numpy() for n, t in w.items()}
         oeq = oracle.mlp(oracle.trippool(oq, omask), wn["w1q"], wn["b1q"], wn["w2q"], wn["b2q"])
         oek = oracle.mlp(oracle.trippool(ok_, omask), wn["w1k"], wn["b1k"], wn["w2k"], wn["b2k"])
@@ -355,9 +412,12 @@ def test_waver_full_size_sampled(V, oracle):
         NT = 1920
         boundary = [i for i in range(NT) if ocnt[0, i] < 128]
         units = sorted(set(rng.choice(NT, 40, replace=False).tolist() + boundary[:4] + boundary[-4:]))
-        check_attention(oracle, oq, ok_, ov, got, omask, u16(path.ot[h:h + 1]), units=units, tag=f"waver h{h}")
-    # untiling of every head is the exact inverse of tiling
-    assert torch.equal(V.tile_unpermute(path.qt, pre.lat, [pre.cfg]), q)
+        # the path stores token order: tile the GPU output with the oracle's tiling
+        o_t, _, _ = oracle.tile_permute(u16(o[h:h + 1]), pre.lat, [pre.cfg])
+        check_attention(oracle, oq, ok_, ov, got, omask, o_t, units=units, tag=f"waver h{h}")
+    # tiling of every head: permute then untile is the identity at full size
+    qt, _, _ = V.tile_permute(q, pre.lat, [pre.cfg], meta=False)
+    assert torch.equal(V.tile_unpermute(qt, pre.lat, [pre.cfg]), q)
 
 
 def test_alt_schedule_1q_parity():
@@ -370,7 +430,8 @@ def test_alt_schedule_1q_parity():
     here = os.path.dirname(os.path.abspath(__file__))
     env = dict(os.environ, VEDA_ATTN="1q")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_parity.py"),
-                        "-k", "test_attention_vs_oracle or test_dense_k_equals_nt or test_random_lists_and_small_k or test_end_to_end_path_object"],
+                        "-k", "test_attention_vs_oracle or test_dense_k_equals_nt or test_random_lists_and_small_k or "
+                        "(test_end_to_end_path_object and tiled)"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 

@@ -29,7 +29,7 @@ def main():
     heads = list(range(a.heads))
     q, k, v = synth.qkv(pre, heads=heads, device=dev)
     w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, heads=heads).items()}
-    path = veda.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev)
+    path = veda.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev, mode="tiled")
     path(q, k, v)
     idx = path.idx
     if a.regime == "dense_seq":

@@ -26,7 +26,7 @@ def main():
     heads = list(range(a.heads))
     q, k, v = synth.qkv(pre, heads=heads, device=dev)
     w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, heads=heads).items()}
-    path = veda.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev)
+    path = veda.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev, mode="tiled")
     path(q, k, v)
     tr = torch.zeros(16 * 128 * 8, dtype=torch.int64, device=dev)
     lib.veda_dbg_set_attn_trace(ctypes.c_void_p(tr.data_ptr()))

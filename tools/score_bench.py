@@ -26,7 +26,7 @@ def main(name="waver12b"):
     dev = torch.device("cuda")
     q, k, v = synth.qkv(pre, device=dev)
     w = {n: t.to(dev) for n, t in synth.scorer_weights(pre).items()}
-    path = veda.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity, device=dev)
+    path = veda.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity, device=dev, mode="tiled")
     path(q, k, v)
     Hh, NT = pre.heads, path.shape.n_tiles
     din, dh, dl = 3 * pre.d, w["w1q"].shape[-1], w["w2q"].shape[-1]

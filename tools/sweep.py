@@ -56,7 +56,7 @@ def main():
         out = torch.empty_like(q)
         dense_ms = None
         for sp in SPARSITIES:
-            path = veda.SparseAttention(lat, [pre.cfg], heads, 128, w, sparsity=sp, device=dev)
+            path = veda.SparseAttention(lat, [pre.cfg], heads, 128, w, sparsity=sp, device=dev, mode="tiled")
             NT, B = path.shape.n_tiles, path.shape.B
             call_ms = timeit(lambda: path(q, k, v, out=out), a.reps)
             attn_ms = timeit(lambda: veda.sparse_attn_fwd(path.qt, path.kt, path.vt, path.idx, path.mask, out=path.ot),

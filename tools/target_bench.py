@@ -38,7 +38,7 @@ def main():
     dev = torch.device("cuda")
     q, k, v = synth.qkv(pre, heads=range(a.heads), device=dev)
     w = {n: t[:a.heads].contiguous().to(dev) for n, t in synth.scorer_weights(pre).items()}
-    path = veda.SparseAttention(pre.lat, [pre.cfg], a.heads, pre.d, w, sparsity=pre.sparsity)
+    path = veda.SparseAttention(pre.lat, [pre.cfg], a.heads, pre.d, w, sparsity=pre.sparsity, mode="tiled")
     path(q, k, v)
     qt, kt, vt, mask, cnt = path.qt, path.kt, path.vt, path.mask, path.cnt
     Hh, NT, B, d = qt.shape
