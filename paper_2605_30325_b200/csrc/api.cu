@@ -162,6 +162,15 @@ veda_status shape_of(veda_latent lat, const veda_tile_cfg *cfg, int Hh, Shape *s
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
+bool scorer_uses_ozaki()
+{
+    static const bool oz = [] {
+        const char *e = getenv("VEDA_SCORER");
+        return !(e && strcmp(e, "dmma") == 0);
+    }();
+    return oz;
+}
+
 namespace {
 
 inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -203,6 +212,7 @@ veda_status veda_tile_score_workspace(int32_t Hh, int32_t n_tiles, int32_t d, co
     b += 2 * align256(rows * w->d_in * sizeof(float));      // Zq, Zk
     b += align256(rows * w->d_hidden * sizeof(double));     // hidden (reused by q and k)
     b += 2 * align256(rows * w->d_lat * sizeof(double));    // Eq, Ek
+    b += ozaki_workspace(Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat);  // int8 slices + row exponents
     *bytes = b;
     return VEDA_OK;
 }
@@ -312,6 +322,12 @@ veda_status veda_tile_score(const uint16_t *q_tiled, const uint16_t *k_tiled, co
     double *ek = reinterpret_cast<double *>(p);
     if ((st = veda_trippool(q_tiled, slot_mask, Hh, n_tiles, B, d, zq, stream)) != VEDA_OK) return st;
     if ((st = veda_trippool(k_tiled, slot_mask, Hh, n_tiles, B, d, zk, stream)) != VEDA_OK) return st;
+    if (scorer_uses_ozaki()) {
+        const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
+        return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq,
+                                  ek, scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),
+                                  S(stream));
+    }
     if ((st = veda_project(zq, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1q, w->b1q, w->w2q, w->b2q, hid, eq,
                            stream)) != VEDA_OK)
         return st;
@@ -340,6 +356,12 @@ veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32
     double *hid = reinterpret_cast<double *>(p); p += align256(rows * w->d_hidden * sizeof(double));
     double *eq = reinterpret_cast<double *>(p); p += align256(rows * w->d_lat * sizeof(double));
     double *ek = reinterpret_cast<double *>(p);
+    if (scorer_uses_ozaki()) {
+        const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
+        return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq,
+                                  ek, scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),
+                                  S(stream));
+    }
     if ((st = veda_project(zq, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1q, w->b1q, w->w2q, w->b2q, hid, eq,
                            stream)) != VEDA_OK)
         return st;

@@ -73,6 +73,13 @@ veda_status launch_sparse_attn_tok(const uint16_t *q, const uint16_t *k, const u
 veda_status launch_tile_pool_tokens(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfgs &cf, int Hh, int Tp,
                                     int Hp, int Wp, int T, int H, int W, int B, int NT, int d, float *z,
                                     int32_t *cnt, uint32_t *mask, cudaStream_t s);
+// scorer GEMMs on the INT8 tensor cores (ozaki.cu); w_q / w_k = {w1, b1, w2, b2}
+size_t ozaki_workspace(int Hh, int NT, int din, int dh, int dl);
+veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *cnt, int Hh, int NT, int din, int dh,
+                               int dl, const float *const w_q[4], const float *const w_k[4], double *hidden,
+                               double *eq, double *ek, float *scores, void *scratch, cudaStream_t s);
+// true unless VEDA_SCORER=dmma (the FP64 tensor-core GEMMs of score.cu) is set at load
+bool scorer_uses_ozaki();
 veda_status launch_sparse_attn_1q(const uint16_t *q, const uint16_t *k, const uint16_t *v, const int32_t *idx,
                                   const uint32_t *mask, int Hh, int NT, int B, int d, int kk, float scale,
                                   uint16_t *o, float *lse, cudaStream_t s);

@@ -78,15 +78,15 @@ def run(request, V, oracle):
     zq, zk = V.trippool(qt, mask), V.trippool(kt, mask)
     eq = V.project(zq, w["w1q"], w["b1q"], w["w2q"], w["b2q"])
     ek = V.project(zk, w["w1k"], w["b1k"], w["w2k"], w["b2k"])
-    s = V.pair_scores(eq, ek, cnt)
-    s_fused = V.tile_score(qt, kt, cnt, mask, V.make_scorer(w))
+    s_sub = V.pair_scores(eq, ek, cnt)  # FP64-tensor-core sub-steps (veda_project / veda_pair_scores)
+    s = V.tile_score(qt, kt, cnt, mask, V.make_scorer(w))  # the path's scorer (INT8 Ozaki, ozaki.cu)
     idx = V.select_topk(s, kk)
     o_t, lse = V.sparse_attn_fwd(qt, kt, vt, idx, mask, want_lse=True)
     o = V.tile_unpermute(o_t, c.lat, c.cfgs)
     torch.cuda.synchronize()
     r.update(dict(qt=u16(qt), kt=u16(kt), vt=u16(vt), cnt=cnt.cpu().numpy(), mask=bits32(mask), zq=zq.cpu().numpy(),
                   zk=zk.cpu().numpy(), eq=eq.cpu().numpy(), ek=ek.cpu().numpy(), s=s.cpu().numpy(),
-                  s_fused=s_fused.cpu().numpy(), idx=idx.cpu().numpy(), o_t=u16(o_t), lse=lse.cpu().numpy(),
+                  s_sub=s_sub.cpu().numpy(), idx=idx.cpu().numpy(), o_t=u16(o_t), lse=lse.cpu().numpy(),
                   o=u16(o), k=kk, NT=NT))
     # oracle from the same bf16 inputs
     oq, ocnt, omask = oracle.tile_permute(u16(c.q), c.lat, c.cfgs)
@@ -127,12 +127,16 @@ def test_projection_and_scores_same_inputs(run, oracle):
     e_or = oracle.mlp(run["zq"].astype(np.float64), w["w1q"], w["b1q"], w["w2q"], w["b2q"])
     assert np.allclose(run["eq"], e_or, rtol=1e-12, atol=1e-12)
     s_or = oracle.scores(run["eq"], run["ek"], run["cnt"]).astype(np.float32)
-    g = run["s"]
+    g = run["s_sub"]
     assert np.array_equal(np.isneginf(g), np.isneginf(s_or))
     fin = np.isfinite(s_or)
     ulps = np.abs(g[fin].view(np.int32).astype(np.int64) - s_or[fin].view(np.int32).astype(np.int64))
     assert ulps.max() <= 1
-    assert np.array_equal(run["s"], run["s_fused"])  # veda_tile_score == its sub-steps
+    # veda_tile_score (INT8 Ozaki GEMMs) vs its FP64 sub-steps: both fp64-accurate
+    a, b = run["s"], run["s_sub"]
+    assert np.array_equal(np.isneginf(a), np.isneginf(b))
+    rel = np.abs(a[fin].astype(np.float64) - b[fin]) / np.maximum(1.0, np.abs(b[fin]))
+    assert rel.max() < 2e-7, rel.max()
 
 
 def test_scores_end_to_end(run):
@@ -482,3 +486,45 @@ def test_host_pipeline_one_shot_api(V):
     want = V.sparse_attention(c.q.to(dev), c.k.to(dev), c.v.to(dev), c.lat, c.cfgs,
                               {n: t.to(dev) for n, t in c.w.items()}, k_keep=c.k_keep).cpu()
     assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+
+
+_SCORER_SNIPPET = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2605_30325_b200 import synth, veda
+veda.load()
+pre = synth.PRESETS["waver12b"]
+dev = torch.device("cuda")
+heads = [0, 1, 2]
+q, k, v = synth.qkv(pre, heads=heads, device=dev)
+w = {{n: t.to(dev) for n, t in synth.scorer_weights(pre, heads=heads, random_bias=True).items()}}
+path = veda.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev)
+path(q, k, v)
+torch.cuda.synchronize()
+np.save({out!r}, path.scores.cpu().numpy())
+"""
+
+
+def test_scorer_int8_ozaki_vs_fp64_dmma(tmp_path):
+    """The INT8-tensor-core scorer (ozaki.cu, default) against the FP64-tensor-core scorer
+    (VEDA_SCORER=dmma) on three full-size Waver heads: both are fp64-accurate, so the fp32
+    scores agree to ~1 ulp (bound 2e-7 relative, far inside the 1e-5 near-tie window)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("ozaki", "dmma"):
+        out = str(tmp_path / f"s_{mode}.npy")
+        env = dict(os.environ, VEDA_SCORER=mode)
+        r = subprocess.run([sys.executable, "-c", _SCORER_SNIPPET.format(root=root, out=out)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs[mode] = np.load(out)
+    a, b = outs["ozaki"], outs["dmma"]
+    assert np.array_equal(np.isfinite(a), np.isfinite(b))
+    fin = np.isfinite(a)
+    rel = np.abs(a[fin].astype(np.float64) - b[fin]) / np.maximum(1.0, np.abs(b[fin]))
+    print(f"ozaki vs dmma: max rel {rel.max():.3e}, identical {np.mean(a[fin] == b[fin]) * 100:.2f} %")
+    assert rel.max() < 2e-7
