@@ -17,12 +17,13 @@
 //   Simulated on the Waver synthetic heads (fp64 reference): max |S error| 1.0e-8 with
 //   NS = 5 (1.3e-6 with NS = 4), vs 7.9e-7 for fp32-stored phi.
 //
-// Kernels: split_rows / split_cols (row or column digits of an fp32/fp64 matrix; int8
-// slices [batch][NS][R][Kp], Kp = K rounded up to 64, zero padded) and oz_gemm_kernel
-// (one 128 x BN output tile per CTA; warp 0 TMA producer, warp 1 tcgen05 issuer, all four
-// warps the epilogue; 3-stage ring of 64-byte K slabs, SWIZZLE_64B, all five A and B
-// slices of a slab in one 4-D TMA box each; epilogues: +bias and erf-GELU -> fp64 hidden,
-// +bias -> fp64 phi, /sqrt(d') with -inf for empty key tiles -> fp32 S).
+// Kernels: split_rows / split_cols (row or column digits of an fp32/fp64 matrix, from a
+// 35-bit fixed-point rounding; int8 slices [batch][NS][R][Kp], Kp = K rounded up to 64,
+// zero padded; split_rows optionally applies the erf-GELU of layer 1 first) and the
+// persistent oz_gemm_kernel (128 x BN output tiles; warp 0 TMA producer, warp 1 tcgen05
+// issuer, warps 2-5 epilogue; 3-stage ring of 64-byte K slabs, SWIZZLE_64B, all five A and
+// B slices of a slab in one 4-D TMA box each; epilogues: +bias -> fp64 (layer-1
+// pre-activation, phi), x 1/sqrt(d') with -inf for empty key tiles -> fp32 S).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -43,7 +44,7 @@ constexpr int BM = 128;     // output rows per CTA (TMEM lanes)
 constexpr int BKB = 64;     // K bytes per stage (one SWIZZLE_64B row)
 constexpr int NSTAGE = 3;
 
-enum { EPI_GELU_BIAS = 0, EPI_BIAS = 1, EPI_SCORE = 2 };
+enum { EPI_BIAS = 1, EPI_SCORE = 2 };
 
 // ---------------------------------------------------------------- splitting
 __device__ __forceinline__ int row_exponent(double m)
@@ -53,63 +54,122 @@ __device__ __forceinline__ int row_exponent(double m)
     return e;
 }
 
-// the NS digits of x (|x| < 2^e), packed: digit s of value q goes to byte q of word s
+// The NS digits of x (|x| < 2^e): Y = rint(x 2^(34-e)) is a 35-bit fixed-point integer
+// (|Y| <= 2^34, error <= 2^(e-35)); balanced base-128 digits are peeled off from the low
+// end, a_4 .. a_1 in [-64, 63], and a_0 = the rest (|a_0| <= 64), so
+// x ~ 2^e sum_s a_s 2^-(7s+6).  Digit s of value q goes to byte q of word s.
 __device__ __forceinline__ void digits4(const double (&x)[4], int e, uint32_t (&w)[NS])
 {
+    const double scale = __longlong_as_double((long long)(1023 + 34 - e) << 52);  // 2^(34-e)
 #pragma unroll
     for (int s = 0; s < NS; ++s) w[s] = 0u;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        double y = ldexp(x[q], -e);  // exact, |y| < 1
+        long long Y = __double2ll_rn(x[q] * scale);
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-            y *= (s == 0) ? 64.0 : 128.0;
-            const double a = rint(y);
-            y -= a;  // exact
-            w[s] |= (uint32_t)(uint8_t)(int8_t)(int)a << (8 * q);
+        for (int s = NS - 1; s > 0; --s) {
+            const int d = (int)((Y + 64) & 127) - 64;
+            Y = (Y - d) >> 7;
+            w[s] |= (uint32_t)(uint8_t)(int8_t)d << (8 * q);
         }
+        w[0] |= (uint32_t)(uint8_t)(int8_t)(int)Y << (8 * q);
     }
 }
 
-// A row per warp, K contiguous (element (b, r, k) at X[b*sb + r*sr + k])
-template <typename T>
+// GELU(x) = x Phi(x) (erf form, reading R8) in fp64 without the libdevice erf (which costs
+// ~70 FP64 instructions and made the layer-2 split FP64-bound): Phi on [-8, 8] from a
+// table of degree-9 Taylor polynomials around the centres of 256 intervals of width 1/16
+// (truncation error < 1e-16 relative; coefficients from Phi(c) = erfc(-c/sqrt2)/2 and
+// Phi^(n+1)(c) = (-1)^n He_n(c) phi(c), built once on the host); |x| >= 8: Phi = 0 or 1
+// (error < 7e-16).
+constexpr int PHI_N = 256, PHI_DEG = 9;  // PHI_DEG + 1 coefficients, read as double2 pairs
+__device__ __align__(16) double g_phi_tab[PHI_N][PHI_DEG + 1];
+
+__device__ __forceinline__ double gelu_tab(double x, const double2 (*tab)[(PHI_DEG + 1) / 2])
+{
+    if (x >= 8.0) return x;
+    if (x <= -8.0) return 0.0;
+    int i = (int)((x + 8.0) * 16.0);
+    if (i > PHI_N - 1) i = PHI_N - 1;
+    const double h = x - (-8.0 + (i + 0.5) / 16.0);
+    const double2 *c = tab[i];
+    double2 q = c[(PHI_DEG + 1) / 2 - 1];
+    double p = fma(q.y, h, q.x);
+#pragma unroll
+    for (int n = (PHI_DEG + 1) / 2 - 2; n >= 0; --n) {
+        q = c[n];
+        p = fma(fma(p, h, q.y), h, q.x);
+    }
+    return x * p;
+}
+
+// A row per warp, K contiguous (element (b, r, k) at X[b*sb + r*sr + k]); the row is held
+// in registers (J x 4 values per lane, K <= 128 J).  GELU: the row is the layer-1
+// pre-activation and the digits are those of GELU(x) (erf form, reading R8).
+template <typename T, int J, bool GELU>
 __global__ void __launch_bounds__(256) split_rows_kernel(const T *__restrict__ X, int R, int K, int64_t sr,
                                                          int64_t sb, int Kp, int8_t *__restrict__ out,
                                                          int32_t *__restrict__ ex)
 {
-    const int lane = threadIdx.x & 31;
-    const int r = blockIdx.x * 8 + (threadIdx.x >> 5), b = blockIdx.y;
-    if (r >= R) return;
-    const T *x = X + b * sb + (int64_t)r * sr;
-    double m = 0.0;
-    for (int k = lane; k < K; k += 32) m = fmax(m, fabs((double)__ldg(x + k)));
+    // GELU: the Phi table is staged in shared memory once per block (grid-stride over rows)
+    __shared__ double2 s_tab[GELU ? PHI_N : 1][(PHI_DEG + 1) / 2];
+    if (GELU) {
+        const double2 *g = reinterpret_cast<const double2 *>(&g_phi_tab[0][0]);
+        double2 *d = &s_tab[0][0];
+        for (int i = threadIdx.x; i < PHI_N * (PHI_DEG + 1) / 2; i += 256) d[i] = g[i];
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31, b = blockIdx.y;
+    for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < R; r += gridDim.x * 8) {
+        const T *x = X + b * sb + (int64_t)r * sr;
+        double v[J][4];
+        double m = 0.0;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-    const int e = row_exponent(m);
-    if (lane == 0) ex[(int64_t)b * R + r] = e;
-    int8_t *o = out + ((int64_t)b * NS * R + r) * Kp;
-    for (int k = lane * 4; k < Kp; k += 128) {
-        double v[4];
+        for (int j = 0; j < J; ++j)  // all loads first (K and the row start are multiples of 4)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = (k + q < K) ? (double)__ldg(x + k + q) : 0.0;
-        uint32_t w[NS];
-        digits4(v, e, w);
+            for (int q = 0; q < 4; ++q) {
+                const int k = 128 * j + 4 * lane + q;
+                v[j][q] = (k < K) ? (double)__ldg(x + k) : 0.0;
+            }
 #pragma unroll
-        for (int s = 0; s < NS; ++s) *reinterpret_cast<uint32_t *>(o + (int64_t)s * R * Kp + k) = w[s];
+        for (int j = 0; j < J; ++j)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (GELU && 128 * j + 4 * lane + q < K) v[j][q] = gelu_tab(v[j][q], s_tab);
+                m = fmax(m, fabs(v[j][q]));
+            }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        const int e = row_exponent(m);
+        if (lane == 0) ex[(int64_t)b * R + r] = e;
+        int8_t *o = out + ((int64_t)b * NS * R + r) * Kp;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int k = 128 * j + 4 * lane;
+            if (k >= Kp) break;
+            uint32_t w[NS];
+            digits4(v[j], e, w);
+#pragma unroll
+            for (int s = 0; s < NS; ++s) *reinterpret_cast<uint32_t *>(o + (int64_t)s * R * Kp + k) = w[s];
+        }
     }
 }
 
 // Matrices stored with the row index contiguous (element (b, r, k) at X[b*sb + k*sk + r]),
-// e.g. W1 [d_in][d_h] read as B^T rows n = 0..d_h-1: a block of 32 rows x 8 k-groups; the
-// row maximum is reduced across the k-groups in shared memory; loads coalesce over rows
+// e.g. W1 [d_in][d_h] read as B^T rows n = 0..d_h-1: a block of 32 rows x 8 k-groups.  The
+// row maximum is reduced across the k-groups in shared memory; loads coalesce over rows;
+// the digits of a 128-wide k chunk are transposed through shared memory so every slice row
+// is written as contiguous 128-byte runs.
 template <typename T>
 __global__ void __launch_bounds__(256) split_cols_kernel(const T *__restrict__ X, int R, int K, int64_t sk,
                                                          int64_t sb, int Kp, int8_t *__restrict__ out,
                                                          int32_t *__restrict__ ex)
 {
     __shared__ double s_m[8][32];
+    __shared__ uint32_t s_d[NS][32][33];  // [slice][row][k word], padded
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int r = blockIdx.x * 32 + tx, b = blockIdx.y;
+    const int r0 = blockIdx.x * 32, b = blockIdx.y;
+    const int r = r0 + tx;
     const bool ok = r < R;
     const T *x = X + b * sb + (ok ? r : 0);
     double m = 0.0;
@@ -119,28 +179,39 @@ __global__ void __launch_bounds__(256) split_cols_kernel(const T *__restrict__ X
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 8; ++j) m = fmax(m, s_m[j][tx]);
-    if (!ok) return;
     const int e = row_exponent(m);
-    if (ty == 0) ex[(int64_t)b * R + r] = e;
-    int8_t *o = out + ((int64_t)b * NS * R + r) * Kp;
-    for (int k = ty * 4; k < Kp; k += 32) {
-        double v[4];
+    if (ty == 0 && ok) ex[(int64_t)b * R + r] = e;
+    for (int kc = 0; kc < Kp; kc += 128) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = (k + q < K) ? (double)__ldg(x + (int64_t)(k + q) * sk) : 0.0;
-        uint32_t w[NS];
-        digits4(v, e, w);
+        for (int j = 0; j < 4; ++j) {  // k words ty + 8j of this chunk: 4 values each
+            const int wk = ty + 8 * j, k = kc + 4 * wk;
+            double v[4];
 #pragma unroll
-        for (int s = 0; s < NS; ++s) *reinterpret_cast<uint32_t *>(o + (int64_t)s * R * Kp + k) = w[s];
+            for (int q = 0; q < 4; ++q) v[q] = (ok && k + q < K) ? (double)__ldg(x + (int64_t)(k + q) * sk) : 0.0;
+            uint32_t w[NS];
+            digits4(v, e, w);
+#pragma unroll
+            for (int s = 0; s < NS; ++s) s_d[s][tx][wk] = w[s];
+        }
+        __syncthreads();
+        // write: slice s, row rr, word ww (32 words = 128 bytes per row chunk)
+        for (int i = threadIdx.x; i < NS * 32 * 32; i += 256) {
+            const int ww = i & 31, rr = (i >> 5) & 31, s = i >> 10;
+            if (r0 + rr < R && kc + 4 * ww < Kp)
+                *reinterpret_cast<uint32_t *>(out + ((int64_t)(b * NS + s) * R + r0 + rr) * Kp + kc + 4 * ww) =
+                    s_d[s][rr][ww];
+        }
+        __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------- GEMM
 struct GemmArgs {
     const int32_t *ea, *eb;  // row exponents of A [batch][M] and B [batch][N]
-    const float *bias;       // [batch][N] (EPI_GELU_BIAS / EPI_BIAS)
+    const float *bias;       // [batch][N] (EPI_BIAS)
     const int32_t *cnt;      // [batch][N] key-tile counts (EPI_SCORE)
     void *C;                 // [batch][M][N]: fp64 (hidden / phi) or fp32 (scores)
-    int M, N, nk;            // nk = Kp / 64
+    int M, N, nk, batch;     // nk = Kp / 64
     double den;              // EPI_SCORE: sqrt(d')
 };
 
@@ -149,31 +220,45 @@ struct GemmGeo {
     static constexpr int A_BYTES = NS * BM * BKB;
     static constexpr int B_BYTES = NS * BN * BKB;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int SMEM = NSTAGE * STAGE + 1024 + 64;
+    static constexpr int SMEM = NSTAGE * STAGE + 1024 + 128;
     static_assert(NS * BN <= 512, "accumulators exceed TMEM");
 };
 
+// Persistent: one CTA per SM walks the (batch, m-block, n-block) tiles (n fastest, so an
+// A slab is re-read from L2 by the neighbouring tiles).  Warp 0: TMA producer running ahead
+// across tile boundaries through the 3-stage ring; warp 1: MMA issuer (waits until the
+// epilogue has drained the accumulators of the previous tile); warps 2-5: epilogue (warp w
+// reads TMEM lane quarter w % 4), releasing TMEM as soon as the last accumulator chunk is
+// in registers.
+constexpr int GEMM_THREADS = 192;
+
 template <int BN, int EPI>
-__global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                         const __grid_constant__ CUtensorMap tmB, const GemmArgs g)
+__global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                                  const __grid_constant__ CUtensorMap tmB,
+                                                                  const GemmArgs g)
 {
     using G = GemmGeo<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
     const uint32_t sbar = sbase + NSTAGE * G::STAGE;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + NSTAGE * G::STAGE + 8 * (2 * NSTAGE + 1));
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + NSTAGE * G::STAGE + 8 * (2 * NSTAGE + 2));
 #define OZ_FULL(i) (sbar + 8u * (i))
 #define OZ_EMPTY(i) (sbar + 8u * (NSTAGE + (i)))
 #define OZ_DONE (sbar + 8u * (2 * NSTAGE))
+#define OZ_TFREE (sbar + 8u * (2 * NSTAGE + 1))
+    __shared__ int s_eb[BN];
+    __shared__ double s_col[BN];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, b = blockIdx.z;
+    const int nmb = (g.M + BM - 1) / BM, nnb = (g.N + BN - 1) / BN;
+    const int ntiles = nmb * nnb * g.batch;
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
             mbar_init(OZ_FULL(i), 1);
             mbar_init(OZ_EMPTY(i), 1);
         }
         mbar_init(OZ_DONE, 1);
+        mbar_init(OZ_TFREE, 128);
         fence_barrier_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
@@ -186,118 +271,139 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    auto tile_coords = [&](int t, int &b, int &m0, int &n0) {
+        const int nb = t % nnb, r = t / nnb;
+        m0 = (r % nmb) * BM;
+        b = r / nmb;
+        n0 = nb * BN;
+    };
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer: all NS slices of A and of B for one 64-byte K slab
-            for (int kc = 0; kc < g.nk; ++kc) {
-                const int st = kc % NSTAGE;
-                const uint32_t ph = (uint32_t)(kc / NSTAGE) & 1u;
-                mbar_wait(OZ_EMPTY(st), ph ^ 1u);
-                mbar_expect_tx(OZ_FULL(st), G::STAGE);
-                const uint32_t sa = sbase + st * G::STAGE;
-                tma_load_4d(sa, &tmA, kc * BKB, m0, 0, b, OZ_FULL(st));
-                tma_load_4d(sa + G::A_BYTES, &tmB, kc * BKB, n0, 0, b, OZ_FULL(st));
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int b, m0, n0;
+                tile_coords(t, b, m0, n0);
+                for (int kc = 0; kc < g.nk; ++kc, ++it) {
+                    const int st = it % NSTAGE;
+                    mbar_wait(OZ_EMPTY(st), ((uint32_t)(it / NSTAGE) & 1u) ^ 1u);
+                    mbar_expect_tx(OZ_FULL(st), G::STAGE);
+                    const uint32_t sa = sbase + st * G::STAGE;
+                    tma_load_4d(sa, &tmA, kc * BKB, m0, 0, b, OZ_FULL(st));
+                    tma_load_4d(sa + G::A_BYTES, &tmB, kc * BKB, n0, 0, b, OZ_FULL(st));
+                }
             }
         }
         __syncwarp();
     } else if (warp == 1) {  // MMA issuer (warp-uniform loop, one elected lane issues)
         constexpr uint32_t idesc = idesc_s8_s32(BM, BN);
-        for (int kc = 0; kc < g.nk; ++kc) {
-            const int st = kc % NSTAGE;
-            mbar_wait(OZ_FULL(st), (uint32_t)(kc / NSTAGE) & 1u);
+        int it = 0, nt = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+            mbar_wait(OZ_TFREE, ((uint32_t)nt & 1u) ^ 1u);  // accumulators drained by the epilogue
             tc_fence_after();
-            const uint32_t sa = sbase + st * G::STAGE, sb = sa + G::A_BYTES;
+            for (int kc = 0; kc < g.nk; ++kc, ++it) {
+                const int st = it % NSTAGE;
+                mbar_wait(OZ_FULL(st), (uint32_t)(it / NSTAGE) & 1u);
+                tc_fence_after();
+                const uint32_t sa = sbase + st * G::STAGE, sb = sa + G::A_BYTES;
 #pragma unroll
-            for (int kk = 0; kk < BKB / 32; ++kk) {
+                for (int kk = 0; kk < BKB / 32; ++kk) {
 #pragma unroll
-                for (int s = 0; s < NS; ++s) {
-                    const uint64_t ad = sdesc_sw64(sa + s * BM * BKB + kk * 32, 512);
+                    for (int s = 0; s < NS; ++s) {
+                        const uint64_t ad = sdesc_sw64(sa + s * BM * BKB + kk * 32, 512);
 #pragma unroll
-                    for (int t = 0; t + s < NS; ++t) {
-                        const uint64_t bd = sdesc_sw64(sb + t * BN * BKB + kk * 32, 512);
-                        mma_i8_ss_w(tbase + (uint32_t)((s + t) * BN), ad, bd, idesc,
-                                    (kc > 0 || kk > 0 || s > 0) ? 1u : 0u);
+                        for (int tt = 0; tt + s < NS; ++tt) {
+                            const uint64_t bd = sdesc_sw64(sb + tt * BN * BKB + kk * 32, 512);
+                            mma_i8_ss_w(tbase + (uint32_t)((s + tt) * BN), ad, bd, idesc,
+                                        (kc > 0 || kk > 0 || s > 0) ? 1u : 0u);
+                        }
                     }
                 }
+                tc_commit_w(OZ_EMPTY(st));
             }
-            tc_commit_w(OZ_EMPTY(st));
+            tc_commit_w(OZ_DONE);
         }
-        tc_commit_w(OZ_DONE);
         __syncwarp();
-    }
-    // ---- epilogue (all four warps; warp w owns TMEM lanes / tile rows 32w .. 32w+31).
-    // Per-column data (exponent of B's row, bias or key-tile count) staged in smem once per
-    // tile: read from global inside the element loop, the loads could not be hoisted above
-    // the output stores (possible aliasing) and serialised the epilogue.
-    __shared__ int s_eb[BN];
-    __shared__ double s_col[BN];
-    for (int c = threadIdx.x; c < BN; c += 128) {
-        const int n = n0 + c;
-        const bool ok = n < g.N;
-        s_eb[c] = ok ? __ldg(g.eb + (int64_t)b * g.N + n) : 0;
-        if (EPI == EPI_SCORE)
-            s_col[c] = (ok && __ldg(g.cnt + (int64_t)b * g.N + n) != 0) ? 1.0 / g.den : -INFINITY;
-        else
-            s_col[c] = ok ? (double)__ldg(g.bias + (int64_t)b * g.N + n) : 0.0;
-    }
-    __syncthreads();
-    mbar_wait(OZ_DONE, 0);
-    tc_fence_after();
-    const int row = warp * 32 + lane, m = m0 + row;
-    const bool mok = m < g.M;
-    const int ea = mok ? __ldg(g.ea + (int64_t)b * g.M + m) : 0;
-    const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
+    } else {  // ---- epilogue warps 2-5
+        const int q = warp & 3;  // TMEM lane quarter (rows 32q .. 32q+31)
+        const int row = q * 32 + lane;
+        const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
+        int nt = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+            int b, m0, n0;
+            tile_coords(t, b, m0, n0);
+            // per-column data of this tile (exponent of B's row, bias / score factor) in smem
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's readers are done
+            for (int c = threadIdx.x - 64; c < BN; c += 128) {
+                const int n = n0 + c;
+                const bool ok = n < g.N;
+                s_eb[c] = ok ? __ldg(g.eb + (int64_t)b * g.N + n) : 0;
+                if (EPI == EPI_SCORE)
+                    s_col[c] = (ok && __ldg(g.cnt + (int64_t)b * g.N + n) != 0) ? 1.0 / g.den : -INFINITY;
+                else
+                    s_col[c] = ok ? (double)__ldg(g.bias + (int64_t)b * g.N + n) : 0.0;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int m = m0 + row;
+            const bool mok = m < g.M;
+            const int ea = mok ? __ldg(g.ea + (int64_t)b * g.M + m) : 0;
+            mbar_wait(OZ_DONE, (uint32_t)nt & 1u);
+            tc_fence_after();
+            const int64_t orow = ((int64_t)b * g.M + m) * g.N;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t acc[NS][16];
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                uint32_t acc[NS][16];
 #pragma unroll
-        for (int u = 0; u < NS; ++u) tmem_ld16(tl + (uint32_t)(u * BN + c0), acc[u]);
-        tmem_wait_ld();
-        if (!mok) continue;
-        const int64_t orow = ((int64_t)b * g.M + m) * g.N;
-        // vector stores only when the whole 16-column run is in range and the row base is aligned
-        const bool full = n0 + c0 + 16 <= g.N && (g.N % 4) == 0;
-        double out[16];
+                for (int u = 0; u < NS; ++u) tmem_ld16(tl + (uint32_t)(u * BN + c0), acc[u]);
+                tmem_wait_ld();
+                if (c0 + 16 >= BN) {  // every accumulator column is in registers: TMEM may be reused
+                    tc_fence_before();
+                    mbar_arrive(OZ_TFREE);
+                }
+                if (!mok) continue;
+                // vector stores only when the whole 16-column run is in range and aligned
+                const bool full = n0 + c0 + 16 <= g.N && (g.N % 4) == 0;
+                double out[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            // sum_u acc_u 2^-(7u+12) = 2^-40 * sum_u acc_u 2^(7(4-u)): |acc_u| < 2^24, so the
-            // weighted sum is an exact int64 below 2^53 and converts to fp64 exactly
-            int64_t iv = 0;
+                for (int i = 0; i < 16; ++i) {
+                    // sum_u acc_u 2^-(7u+12) = 2^-40 * sum_u acc_u 2^(7(4-u)): |acc_u| < 2^24, so
+                    // the weighted sum is an exact int64 below 2^53 and converts to fp64 exactly
+                    int64_t iv = 0;
 #pragma unroll
-            for (int u = 0; u < NS; ++u) iv += (int64_t)(int32_t)acc[u][i] << (7 * (NS - 1 - u));
-            const int sc = ea + s_eb[c0 + i] - (7 * (NS - 1) + 12) + 1023;  // biased exponent of the scale
-            const double v = (double)iv * __longlong_as_double((long long)sc << 52);
-            if (EPI == EPI_GELU_BIAS) {
-                const double x = v + s_col[c0 + i];
-                out[i] = 0.5 * x * (1.0 + erf(x * 0.70710678118654752440));
-            } else if (EPI == EPI_BIAS) {
-                out[i] = v + s_col[c0 + i];
-            } else {
-                const double f = s_col[c0 + i];  // 1/sqrt(d'), or -inf for an empty key tile
-                out[i] = (f == -INFINITY) ? -INFINITY : v * f;
-            }
-        }
-        if (EPI == EPI_SCORE) {
-            float *dst = static_cast<float *>(g.C) + orow + n0 + c0;
-            if (full) {
+                    for (int u = 0; u < NS; ++u) iv += (int64_t)(int32_t)acc[u][i] << (7 * (NS - 1 - u));
+                    const int sc = ea + s_eb[c0 + i] - (7 * (NS - 1) + 12) + 1023;  // biased exponent
+                    const double v = (double)iv * __longlong_as_double((long long)sc << 52);
+                    if (EPI == EPI_SCORE) {
+                        const double f = s_col[c0 + i];  // 1/sqrt(d'), or -inf for an empty key tile
+                        out[i] = (f == -INFINITY) ? -INFINITY : v * f;
+                    } else {
+                        out[i] = v + s_col[c0 + i];  // + bias (layer 1: pre-activation; GELU in the split)
+                    }
+                }
+                if (EPI == EPI_SCORE) {
+                    float *dst = static_cast<float *>(g.C) + orow + n0 + c0;
+                    if (full) {
 #pragma unroll
-                for (int i = 0; i < 16; i += 4)
-                    *reinterpret_cast<float4 *>(dst + i) =
-                        make_float4((float)out[i], (float)out[i + 1], (float)out[i + 2], (float)out[i + 3]);
-            } else {
+                        for (int i = 0; i < 16; i += 4)
+                            *reinterpret_cast<float4 *>(dst + i) =
+                                make_float4((float)out[i], (float)out[i + 1], (float)out[i + 2], (float)out[i + 3]);
+                    } else {
 #pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (n0 + c0 + i < g.N) dst[i] = (float)out[i];
-            }
-        } else {
-            double *dst = static_cast<double *>(g.C) + orow + n0 + c0;
-            if (full) {
+                        for (int i = 0; i < 16; ++i)
+                            if (n0 + c0 + i < g.N) dst[i] = (float)out[i];
+                    }
+                } else {
+                    double *dst = static_cast<double *>(g.C) + orow + n0 + c0;
+                    if (full) {
 #pragma unroll
-                for (int i = 0; i < 16; i += 2) *reinterpret_cast<double2 *>(dst + i) = make_double2(out[i], out[i + 1]);
-            } else {
+                        for (int i = 0; i < 16; i += 2)
+                            *reinterpret_cast<double2 *>(dst + i) = make_double2(out[i], out[i + 1]);
+                    } else {
 #pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (n0 + c0 + i < g.N) dst[i] = out[i];
+                        for (int i = 0; i < 16; ++i)
+                            if (n0 + c0 + i < g.N) dst[i] = out[i];
+                    }
+                }
             }
         }
     }
@@ -310,6 +416,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
 #undef OZ_FULL
 #undef OZ_EMPTY
 #undef OZ_DONE
+#undef OZ_TFREE
 }
 
 // ---------------------------------------------------------------- host side
@@ -317,12 +424,22 @@ veda_status make_slices_map(CUtensorMap *map, const int8_t *base, int rows, int 
 
 int kpad(int K) { return (K + BKB - 1) / BKB * BKB; }
 
-template <typename T>
+template <typename T, bool GELU = false>
 veda_status split_rows(const T *X, int R, int K, int64_t sr, int64_t sb, int batch, int8_t *out, int32_t *ex,
                        cudaStream_t s)
 {
     dim3 grid((R + 7) / 8, batch);
-    split_rows_kernel<T><<<grid, 256, 0, s>>>(X, R, K, sr, sb, kpad(K), out, ex);
+    const int Kp = kpad(K);
+    if (Kp <= 128)
+        split_rows_kernel<T, 1, GELU><<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+    else if (Kp <= 256)
+        split_rows_kernel<T, 2, GELU><<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+    else if (Kp <= 512)
+        split_rows_kernel<T, 4, GELU><<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+    else if (Kp <= 1024)
+        split_rows_kernel<T, 8, GELU><<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+    else
+        return fail(VEDA_ERR_SHAPE, "ozaki scorer: K=%d > 1024 unsupported", K);
     count_launch();
     return check_launch("ozaki split_rows");
 }
@@ -357,8 +474,10 @@ veda_status gemm(const int8_t *As, const int8_t *Bs, int M, int N, int K, int ba
     a.M = M;
     a.N = N;
     a.nk = kpad(K) / BKB;
-    dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
-    oz_gemm_kernel<BN, EPI><<<grid, 128, G::SMEM, s>>>(ma, mb, a);
+    a.batch = batch;
+    const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    oz_gemm_kernel<BN, EPI><<<grid, GEMM_THREADS, G::SMEM, s>>>(ma, mb, a);
     count_launch();
     return check_launch("ozaki gemm");
 }
@@ -387,6 +506,40 @@ veda_status oz::make_slices_map(CUtensorMap *map, const int8_t *base, int rows, 
     return VEDA_OK;
 }
 
+// Taylor table of Phi for gelu_tab, uploaded once per device (static module memory)
+static veda_status phi_table_ready(cudaStream_t s)
+{
+    static bool done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (done[dev]) return VEDA_OK;
+    static double tab[oz::PHI_N][oz::PHI_DEG + 1];
+    const double inv_sqrt2pi = 0.39894228040143267794;
+    for (int i = 0; i < oz::PHI_N; ++i) {
+        const double c = -8.0 + (i + 0.5) / 16.0;
+        const double phi = inv_sqrt2pi * std::exp(-0.5 * c * c);
+        tab[i][0] = 0.5 * std::erfc(-c / std::sqrt(2.0));
+        // He_0 = 1, He_1 = c, He_{n+1} = c He_n - n He_{n-1};  coefficient of h^(n+1): (-1)^n He_n phi / (n+1)!
+        double he_prev = 1.0, he = c, fact = 1.0;
+        for (int n = 0; n < oz::PHI_DEG; ++n) {
+            const double hen = (n == 0) ? 1.0 : (n == 1 ? c : he);
+            fact *= (double)(n + 1);
+            tab[i][n + 1] = ((n & 1) ? -1.0 : 1.0) * hen * phi / fact;
+            if (n >= 1) {
+                const double next = c * he - (double)n * he_prev;
+                he_prev = he;
+                he = next;
+            }
+        }
+    }
+    const cudaError_t e = cudaMemcpyToSymbolAsync(oz::g_phi_tab, tab, sizeof tab, 0, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "ozaki: Phi table upload: %s", cudaGetErrorString(e));
+    if (cudaStreamSynchronize(s) != cudaSuccess) return fail(VEDA_ERR_CUDA, "ozaki: Phi table upload failed");
+    done[dev] = true;
+    return VEDA_OK;
+}
+
 size_t ozaki_workspace(int Hh, int NT, int din, int dh, int dl)
 {
     const size_t k1 = oz::kpad(din), k2 = oz::kpad(dh), k3 = oz::kpad(dl);
@@ -412,18 +565,20 @@ veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *
     int32_t *ea = reinterpret_cast<int32_t *>(p); p += align256((size_t)Hh * NT * 4);
     int32_t *eb = reinterpret_cast<int32_t *>(p);
     veda_status st;
+    if ((st = phi_table_ready(s)) != VEDA_OK) return st;
     for (int side = 0; side < 2; ++side) {
         const float *z = side ? zk : zq;
         const float *const *w = side ? w_k : w_q;
         double *e = side ? ek : eq;
-        // layer 1: hidden = GELU(z W1 + b1)
+        // layer 1: pre-activation z W1 + b1
         if ((st = oz::split_rows<float>(z, NT, din, din, (int64_t)NT * din, Hh, As, ea, s)) != VEDA_OK) return st;
         if ((st = oz::split_cols<float>(w[0], dh, din, dh, (int64_t)din * dh, Hh, Bs, eb, s)) != VEDA_OK) return st;
         oz::GemmArgs a{};
-        a.ea = ea; a.eb = eb; a.bias = w[1]; a.C = hidden;
-        if ((st = oz::gemm<96, oz::EPI_GELU_BIAS>(As, Bs, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
-        // layer 2: e = hidden W2 + b2
-        if ((st = oz::split_rows<double>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, s)) != VEDA_OK) return st;
+        a.ea = ea; a.eb = eb; a.bias = w[1]; a.C = hidden;  // pre-activation z W1 + b1
+        if ((st = oz::gemm<96, oz::EPI_BIAS>(As, Bs, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
+        // layer 2: e = GELU(pre) W2 + b2 (the GELU is applied while splitting the rows)
+        if ((st = oz::split_rows<double, true>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, s)) != VEDA_OK)
+            return st;
         if ((st = oz::split_cols<float>(w[2], dl, dh, dl, (int64_t)dh * dl, Hh, Bs, eb, s)) != VEDA_OK) return st;
         a.bias = w[3]; a.C = e;
         if ((st = oz::gemm<64, oz::EPI_BIAS>(As, Bs, NT, dl, dh, Hh, a, s)) != VEDA_OK) return st;
