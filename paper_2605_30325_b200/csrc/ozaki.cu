@@ -44,7 +44,7 @@ constexpr int BM = 128;     // output rows per CTA (TMEM lanes)
 constexpr int BKB = 64;     // K bytes per stage (one SWIZZLE_64B row)
 constexpr int NSTAGE = 3;
 
-enum { EPI_BIAS = 1, EPI_SCORE = 2 };
+enum { EPI_GELU = 0, EPI_BIAS = 1, EPI_SCORE = 2 };
 
 // ---------------------------------------------------------------- splitting
 __device__ __forceinline__ int row_exponent(double m)
@@ -101,6 +101,13 @@ __device__ __forceinline__ double gelu_tab(double x, const double2 (*tab)[(PHI_D
         p = fma(fma(p, h, q.y), h, q.x);
     }
     return x * p;
+}
+
+// the same from the global table (L1-resident) -- used in the layer-1 GEMM epilogue, where
+// it overlaps the next tile's MMAs
+__device__ __forceinline__ double gelu_tab_g(double x)
+{
+    return gelu_tab(x, reinterpret_cast<const double2 (*)[(PHI_DEG + 1) / 2]>(&g_phi_tab[0][0]));
 }
 
 // A row per warp, K contiguous (element (b, r, k) at X[b*sb + r*sr + k]); the row is held
@@ -376,8 +383,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
                     if (EPI == EPI_SCORE) {
                         const double f = s_col[c0 + i];  // 1/sqrt(d'), or -inf for an empty key tile
                         out[i] = (f == -INFINITY) ? -INFINITY : v * f;
+                    } else if (EPI == EPI_GELU) {
+                        out[i] = gelu_tab_g(v + s_col[c0 + i]);  // hidden = GELU(z W1 + b1)
                     } else {
-                        out[i] = v + s_col[c0 + i];  // + bias (layer 1: pre-activation; GELU in the split)
+                        out[i] = v + s_col[c0 + i];  // + bias
                     }
                 }
                 if (EPI == EPI_SCORE) {
@@ -575,10 +584,15 @@ veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *
         if ((st = oz::split_cols<float>(w[0], dh, din, dh, (int64_t)din * dh, Hh, Bs, eb, s)) != VEDA_OK) return st;
         oz::GemmArgs a{};
         a.ea = ea; a.eb = eb; a.bias = w[1]; a.C = hidden;  // pre-activation z W1 + b1
+#ifndef VEDA_GELU_IN_SPLIT
+        if ((st = oz::gemm<96, oz::EPI_GELU>(As, Bs, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
+        if ((st = oz::split_rows<double>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, s)) != VEDA_OK) return st;
+#else
         if ((st = oz::gemm<96, oz::EPI_BIAS>(As, Bs, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
         // layer 2: e = GELU(pre) W2 + b2 (the GELU is applied while splitting the rows)
         if ((st = oz::split_rows<double, true>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, s)) != VEDA_OK)
             return st;
+#endif
         if ((st = oz::split_cols<float>(w[2], dl, dh, dl, (int64_t)dh * dl, Hh, Bs, eb, s)) != VEDA_OK) return st;
         a.bias = w[3]; a.C = e;
         if ((st = oz::gemm<64, oz::EPI_BIAS>(As, Bs, NT, dl, dh, Hh, a, s)) != VEDA_OK) return st;
