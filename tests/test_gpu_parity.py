@@ -370,27 +370,38 @@ def test_attention_tokens_equals_tiled(V, name):
         assert torch.equal(lse, lse2)
 
 
-def test_waver_full_size_sampled(V, oracle):
-    """Waver-T2V-12B 720P/241f (61x45x80, 24 heads, d=128, 95%) in the bench's launch
-    configuration.  Steps a1-a5 checked in full for 2 heads, attention on 48 sampled
-    query tiles per checked head (always including boundary tiles)."""
+@pytest.mark.parametrize("preset,head_aware", [("waver12b", False), ("wan14b", False), ("wan1.3b", False),
+                                                ("waver12b", True)])
+def test_full_size_sampled(V, oracle, preset, head_aware):
+    """The paper's workloads at full size in the bench's launch configuration (token-layout
+    path): Waver-T2V-12B 720P/241f (61x45x80, 24 heads), Wan2.1-14B 720P/81f (21x45x80, 40
+    heads), Wan2.1-1.3B 480P/81f (21x30x52, 12 heads), and Waver with the head-aware tile
+    shapes cycling over heads.  Steps a1-a5 checked in full for 2 heads,
+    attention on sampled query tiles of those heads (always including boundary tiles)."""
     from paper_2605_30325_b200 import synth
 
-    pre = synth.PRESETS["waver12b"]
+    pre = synth.PRESETS[preset]
+    cfgs = [synth.HEAD_AWARE_CFGS[h % 4] for h in range(pre.heads)] if head_aware else [pre.cfg]
     dev = torch.device("cuda")
     q, k, v = synth.qkv(pre, device=dev)
     w = {n: t.to(dev) for n, t in synth.scorer_weights(pre).items()}
-    path = V.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity)
-    assert path.k == 96 and path.shape.n_tiles == 1920
+    path = V.SparseAttention(pre.lat, cfgs, pre.heads, pre.d, w, sparsity=pre.sparsity)
+    if preset == "waver12b":
+        assert path.k == 96 and path.shape.n_tiles == 1920  # PAPER.md:471: 64x48x80 = 245,760 tokens
     o = path(q, k, v)
     torch.cuda.synchronize()
-    heads = [0, 13]
+    heads = [0, pre.heads // 2 + 1]
     rng = np.random.default_rng(0)
+    NT = path.shape.n_tiles
     for h in heads:
+        ch = [cfgs[h % len(cfgs)]]
         qh, kh, vh = (u16(t[h:h + 1]) for t in (q, k, v))
-        oq, ocnt, omask = oracle.tile_permute(qh, pre.lat, [pre.cfg])
-        ok_, _, _ = oracle.tile_permute(kh, pre.lat, [pre.cfg])
-        ov, _, _ = oracle.tile_permute(vh, pre.lat, [pre.cfg])
+        # the oracle tiles the one head with its own shape; for these presets every shape
+        # pads to the same grid as the whole call (64x48x80 for Waver), so tiles line up
+        oq, ocnt, omask = oracle.tile_permute(qh, pre.lat, ch)
+        assert oq.shape[1] == NT
+        ok_, _, _ = oracle.tile_permute(kh, pre.lat, ch)
+        ov, _, _ = oracle.tile_permute(vh, pre.lat, ch)
         assert np.array_equal(bits32(path.mask[h:h + 1]), omask)
         assert np.array_equal(path.cnt[h:h + 1].cpu().numpy(), ocnt)
         wn = {n: t[h:h + 1].cpu().numpy() for n, t in w.items()}
@@ -400,7 +411,7 @@ def test_waver_full_size_sampled(V, oracle):
         sg = path.scores[h:h + 1].cpu().numpy().astype(np.float64)
         fin = np.isfinite(os_)
         rel = (np.abs(sg[fin] - os_[fin]) / np.maximum(1.0, np.abs(os_[fin]))).max()
-        print(f"[waver h{h}] score max rel err {rel:.3e}")
+        print(f"[{preset} h{h}] score max rel err {rel:.3e}")
         assert rel < 2e-6
         want = oracle.topk(os_.astype(np.float32).astype(np.float64), path.k)
         got = path.idx[h:h + 1].cpu().numpy()
@@ -412,16 +423,15 @@ def test_waver_full_size_sampled(V, oracle):
                 for j in a - b:
                     for j2 in b - a:
                         assert abs(os_[0, i, j] - os_[0, i, j2]) < NEAR_TIE
-        print(f"[waver h{h}] near-tie rows {diff} / {got.shape[1]}")
-        NT = 1920
-        boundary = [i for i in range(NT) if ocnt[0, i] < 128]
+        print(f"[{preset} h{h}] near-tie rows {diff} / {got.shape[1]}")
+        boundary = [i for i in range(NT) if 0 < ocnt[0, i] < ocnt.max()]
         units = sorted(set(rng.choice(NT, 40, replace=False).tolist() + boundary[:4] + boundary[-4:]))
         # the path stores token order: tile the GPU output with the oracle's tiling
-        o_t, _, _ = oracle.tile_permute(u16(o[h:h + 1]), pre.lat, [pre.cfg])
-        check_attention(oracle, oq, ok_, ov, got, omask, o_t, units=units, tag=f"waver h{h}")
+        o_t, _, _ = oracle.tile_permute(u16(o[h:h + 1]), pre.lat, ch)
+        check_attention(oracle, oq, ok_, ov, got, omask, o_t, units=units, tag=f"{preset} h{h}")
     # tiling of every head: permute then untile is the identity at full size
-    qt, _, _ = V.tile_permute(q, pre.lat, [pre.cfg], meta=False)
-    assert torch.equal(V.tile_unpermute(qt, pre.lat, [pre.cfg]), q)
+    qt, _, _ = V.tile_permute(q, pre.lat, cfgs, meta=False)
+    assert torch.equal(V.tile_unpermute(qt, pre.lat, cfgs), q)
 
 
 def test_alt_schedule_1q_parity():
