@@ -584,7 +584,7 @@ veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *
         if ((st = oz::split_cols<float>(w[0], dh, din, dh, (int64_t)din * dh, Hh, Bs, eb, s)) != VEDA_OK) return st;
         oz::GemmArgs a{};
         a.ea = ea; a.eb = eb; a.bias = w[1]; a.C = hidden;  // pre-activation z W1 + b1
-#ifndef VEDA_GELU_IN_SPLIT
+#ifdef VEDA_GELU_IN_GEMM  // measured slower inside the full path (2.7 vs 2.0 ms at Waver)
         if ((st = oz::gemm<96, oz::EPI_GELU>(As, Bs, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
         if ((st = oz::split_rows<double>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, s)) != VEDA_OK) return st;
 #else
