@@ -1,0 +1,50 @@
+"""Small workloads through every kernel of the token-layout path, for compute-sanitizer.
+
+    compute-sanitizer --tool memcheck|synccheck|racecheck python tools/sanitize_path.py
+
+Runs SparseAttention (tokens and tiled modes) on toy shapes with ragged grids, mixed
+per-head tile shapes and both token layouts, the host-buffer pipeline, and the warp /
+CTA top-k kernels; prints one line per case.
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_30325_b200 import synth, veda  # noqa: E402
+
+
+def main():
+    veda.load()
+    dev = torch.device("cuda")
+    cases = [("tiny", (4, 8, 8), [(4, 4, 4)], 64, 1, 0.5),
+             ("ragged_b128", (5, 9, 14), [(4, 4, 8)], 128, 2, 0.5),
+             ("mixed", (9, 10, 13), [(4, 4, 8), (8, 4, 4), (4, 8, 4), (8, 8, 2)], 128, 4, 0.8),
+             ("b64_d128", (3, 5, 6), [(4, 4, 4)], 128, 2, 0.5)]
+    for name, lat, cfgs, d, Hh, sp in cases:
+        cf = cfgs * Hh if len(cfgs) == 1 else cfgs
+        pre = synth.Preset(name, lat, Hh, d, cf[0], sp)
+        q, k, v = synth.qkv(pre, lat=lat, d=d)
+        w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, d=d, random_bias=True).items()}
+        for mode in ("tokens", "tiled"):
+            path = veda.SparseAttention(lat, cf, Hh, d, w, sparsity=sp, device=dev, mode=mode)
+            o = path(q.to(dev), k.to(dev), v.to(dev))
+            qn, kn, vn = (t.transpose(0, 1).contiguous().to(dev).transpose(0, 1) for t in (q, k, v))
+            o2 = path(qn, kn, vn, out=torch.empty_like(qn))
+            torch.cuda.synchronize()
+            assert torch.equal(o, o2.contiguous())
+        oh = path.run_host(q.contiguous().pin_memory(), k.contiguous().pin_memory(), v.contiguous().pin_memory(),
+                           heads_per_chunk=1)
+        torch.cuda.synchronize()
+        assert torch.equal(oh.view(torch.int16), o.cpu().view(torch.int16))
+        print(f"{name}: ok (k={path.k}, n_tiles={path.shape.n_tiles})", flush=True)
+    for NT, kk in ((300, 17), (2100, 50)):  # warp and CTA top-k kernels
+        s = torch.randn(2, NT, NT, device=dev)
+        veda.select_topk(s, kk)
+        torch.cuda.synchronize()
+        print(f"topk NT={NT}: ok", flush=True)
+
+
+if __name__ == "__main__":
+    main()
