@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--dense-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--host-chunk", type=int, default=0,
+                    help="heads per chunk of the host pipeline (0 = library default, ceil(Hh/32))")
     ap.add_argument("--cpu-sample-units", type=int, default=24)
     return ap.parse_args()
 
@@ -303,7 +305,7 @@ def run_ours(args):
         oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
         # the C-ABI host entry point: H2D, the five steps and D2H pipelined over head chunks
         def e2e_step():
-            path.run_host(qh, kh, vh, out=oh)
+            path.run_host(qh, kh, vh, out=oh, heads_per_chunk=args.host_chunk)
 
         e2e_step()
         barrier()

@@ -186,7 +186,7 @@ VEDA_API veda_status veda_sparse_attn_fwd_tokens(const uint16_t *q, const uint16
 
 /* Device workspace veda_sparse_attention_host needs (two buffer sets of one head chunk:
  * token-layout Q/K/V/O, tiled Q/K/V/O, counts, masks, scores, index lists, scorer
- * workspace).  heads_per_chunk <= 0 selects the default ceil(Hh/8).                   */
+ * workspace).  heads_per_chunk <= 0 selects the default ceil(Hh/32).                  */
 VEDA_API veda_status veda_sparse_attention_host_workspace(veda_latent lat, const veda_tile_cfg *cfg /* host [Hh] */,
                                                           int32_t Hh, int32_t d, int32_t k,
                                                           const veda_scorer *w /* host */,
