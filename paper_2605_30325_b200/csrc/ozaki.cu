@@ -21,7 +21,7 @@
 // 35-bit fixed-point rounding; int8 slices [batch][NS][R][Kp], Kp = K rounded up to 64,
 // zero padded; split_rows optionally applies the erf-GELU of layer 1 first) and the
 // persistent oz_gemm_kernel (128 x BN output tiles; warp 0 TMA producer, warp 1 tcgen05
-// issuer, warps 2-5 epilogue; 3-stage ring of 64-byte K slabs, SWIZZLE_64B, all five A and
+// issuer, warps 2-9 epilogue; 3-stage ring of 64-byte K slabs, SWIZZLE_64B, all five A and
 // B slices of a slab in one 4-D TMA box each; epilogues: +bias -> fp64 (layer-1
 // pre-activation, phi), x 1/sqrt(d') with -inf for empty key tiles -> fp32 S).
 #include <cuda.h>
@@ -229,15 +229,19 @@ struct GemmGeo {
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr int SMEM = NSTAGE * STAGE + 1024 + 128;
     static_assert(NS * BN <= 512, "accumulators exceed TMEM");
+    static_assert((BN / 2) % 16 == 0, "each epilogue column half is a whole number of 16-column chunks");
 };
 
 // Persistent: one CTA per SM walks the (batch, m-block, n-block) tiles (n fastest, so an
 // A slab is re-read from L2 by the neighbouring tiles).  Warp 0: TMA producer running ahead
 // across tile boundaries through the 3-stage ring; warp 1: MMA issuer (waits until the
-// epilogue has drained the accumulators of the previous tile); warps 2-5: epilogue (warp w
+// epilogue has drained the accumulators of the previous tile); warps 2-9: epilogue, two
+// warps per TMEM lane quarter splitting the tile's columns (so the accumulators drain in
+// half the time and the next tile's MMAs start sooner) (warp w
 // reads TMEM lane quarter w % 4), releasing TMEM as soon as the last accumulator chunk is
 // in registers.
-constexpr int GEMM_THREADS = 192;
+constexpr int EPI_WARPS = 8;
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -265,7 +269,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
             mbar_init(OZ_EMPTY(i), 1);
         }
         mbar_init(OZ_DONE, 1);
-        mbar_init(OZ_TFREE, 128);
+        mbar_init(OZ_TFREE, 32 * EPI_WARPS);
         fence_barrier_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
@@ -331,8 +335,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
             tc_commit_w(OZ_DONE);
         }
         __syncwarp();
-    } else {  // ---- epilogue warps 2-5
+    } else {  // ---- epilogue warps 2-9
         const int q = warp & 3;  // TMEM lane quarter (rows 32q .. 32q+31)
+        const int cbeg = ((warp - 2) >> 2) * (BN / 2), cend = cbeg + BN / 2;  // this warp's column half
         const int row = q * 32 + lane;
         const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
         int nt = 0;
@@ -340,8 +345,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
             int b, m0, n0;
             tile_coords(t, b, m0, n0);
             // per-column data of this tile (exponent of B's row, bias / score factor) in smem
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's readers are done
-            for (int c = threadIdx.x - 64; c < BN; c += 128) {
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");  // previous tile's readers done
+            for (int c = threadIdx.x - 64; c < BN; c += 32 * EPI_WARPS) {
                 const int n = n0 + c;
                 const bool ok = n < g.N;
                 s_eb[c] = ok ? __ldg(g.eb + (int64_t)b * g.N + n) : 0;
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
                 else
                     s_col[c] = ok ? (double)__ldg(g.bias + (int64_t)b * g.N + n) : 0.0;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
             const int m = m0 + row;
             const bool mok = m < g.M;
             const int ea = mok ? __ldg(g.ea + (int64_t)b * g.M + m) : 0;
@@ -358,12 +363,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
             tc_fence_after();
             const int64_t orow = ((int64_t)b * g.M + m) * g.N;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 16) {
+            for (int c0 = cbeg; c0 < cend; c0 += 16) {
                 uint32_t acc[NS][16];
 #pragma unroll
                 for (int u = 0; u < NS; ++u) tmem_ld16(tl + (uint32_t)(u * BN + c0), acc[u]);
                 tmem_wait_ld();
-                if (c0 + 16 >= BN) {  // every accumulator column is in registers: TMEM may be reused
+                if (c0 + 16 >= cend) {  // this warp's accumulator columns are in registers
                     tc_fence_before();
                     mbar_arrive(OZ_TFREE);
                 }
