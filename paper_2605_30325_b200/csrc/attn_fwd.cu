@@ -494,10 +494,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int w = 0; w < G::MW; ++w) mk[w] = __ldg(mbase + (size_t)jn * G::MW + w);
                 if (t + 1 < K) jn = __ldg(il + t + 1);
 
-                const int trs = r * K + t, trr = 1 + slot;
-                if (lane == 0 && quarter == 0) TR(trr, trs, 0);
+                const int trs = r * K + t, trr = 1 + slot * 4 + quarter;  // trace role per softmax warp
+                if (lane == 0) TR(trr, trs, 0);
                 mbar_wait(S_FULL(slot), sf_ph);
-                if (lane == 0 && quarter == 0) TR(trr, trs, 1);
+                if (lane == 0) TR(trr, trs, 1);
                 sf_ph ^= 1;
                 if (lane == 0) DBG("w%d slot%d t%d S ok\n", warp, slot, t);
                 tc_fence_after();
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < B / 32; ++c) reg_fence(sr[c]);
-                if (lane == 0 && quarter == 0) TR(trr, trs, 2);
+                if (lane == 0) TR(trr, trs, 2);
 
                 bool full = true;
 #pragma unroll
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                                        fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
                 const float mnew = fmaxf(m, mx * sl2);
-                if (lane == 0 && quarter == 0) TR(trr, trs, 3);
+                if (lane == 0) TR(trr, trs, 3);
                 // lazy rescale: only when some row of this warp grew its max by > 8 (log2 units)
                 float f = 1.f;
                 bool rescale = false;
@@ -578,11 +578,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                 }
                 l += ls;
-                if (lane == 0 && quarter == 0) TR(trr, trs, 4);
+                if (lane == 0) TR(trr, trs, 4);
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(P_FULL(slot));
-                if (lane == 0 && quarter == 0) TR(trr, trs, 5);
+                if (lane == 0) TR(trr, trs, 5);
                 if (lane == 0) DBG("w%d slot%d t%d P arrive l=%f m=%f\n", warp, slot, t, l, m);
             }
             // ---- epilogue: O / l -> bf16, padded query rows -> 0
