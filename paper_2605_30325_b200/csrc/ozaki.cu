@@ -113,52 +113,63 @@ __device__ __forceinline__ double gelu_tab_g(double x)
 // A row per warp, K contiguous (element (b, r, k) at X[b*sb + r*sr + k]); the row is held
 // in registers (J x 4 values per lane, K <= 128 J).  GELU: the row is the layer-1
 // pre-activation and the digits are those of GELU(x) (erf form, reading R8).
-template <typename T, int J, bool GELU>
+template <typename T, int J, bool GELU, int WPR>
 __global__ void __launch_bounds__(256) split_rows_kernel(const T *__restrict__ X, int R, int K, int64_t sr,
                                                          int64_t sb, int Kp, int8_t *__restrict__ out,
                                                          int32_t *__restrict__ ex)
 {
-    // GELU: the Phi table is staged in shared memory once per block (grid-stride over rows)
+    // WPR warps share a row (each holds J/WPR of its 128-column chunks, fewer registers ->
+    // more resident warps); the row maximum is combined through shared memory.
+    // GELU: the Phi table is staged in shared memory once per block.
+    constexpr int JW = J / WPR, RPB = 8 / WPR;
     __shared__ double2 s_tab[GELU ? PHI_N : 1][(PHI_DEG + 1) / 2];
+    __shared__ double s_max[8];
     if (GELU) {
         const double2 *g = reinterpret_cast<const double2 *>(&g_phi_tab[0][0]);
         double2 *d = &s_tab[0][0];
         for (int i = threadIdx.x; i < PHI_N * (PHI_DEG + 1) / 2; i += 256) d[i] = g[i];
         __syncthreads();
     }
-    const int lane = threadIdx.x & 31, b = blockIdx.y;
-    for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < R; r += gridDim.x * 8) {
-        const T *x = X + b * sb + (int64_t)r * sr;
-        double v[J][4];
-        double m = 0.0;
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, part = wi % WPR, b = blockIdx.y;
+    const int r = blockIdx.x * RPB + wi / WPR;
+    const bool ok = r < R;
+    const T *x = X + b * sb + (int64_t)(ok ? r : 0) * sr;
+    double v[JW][4];
+    double m = 0.0;
 #pragma unroll
-        for (int j = 0; j < J; ++j)  // all loads first (K and the row start are multiples of 4)
+    for (int jj = 0; jj < JW; ++jj)  // all loads first (K and the row start are multiples of 4)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int k = 128 * j + 4 * lane + q;
-                v[j][q] = (k < K) ? (double)__ldg(x + k) : 0.0;
-            }
-#pragma unroll
-        for (int j = 0; j < J; ++j)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (GELU && 128 * j + 4 * lane + q < K) v[j][q] = gelu_tab(v[j][q], s_tab);
-                m = fmax(m, fabs(v[j][q]));
-            }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-        const int e = row_exponent(m);
-        if (lane == 0) ex[(int64_t)b * R + r] = e;
-        int8_t *o = out + ((int64_t)b * NS * R + r) * Kp;
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const int k = 128 * j + 4 * lane;
-            if (k >= Kp) break;
-            uint32_t w[NS];
-            digits4(v[j], e, w);
-#pragma unroll
-            for (int s = 0; s < NS; ++s) *reinterpret_cast<uint32_t *>(o + (int64_t)s * R * Kp + k) = w[s];
+        for (int q = 0; q < 4; ++q) {
+            const int k = 128 * (part + WPR * jj) + 4 * lane + q;
+            v[jj][q] = (ok && k < K) ? (double)__ldg(x + k) : 0.0;
         }
+#pragma unroll
+    for (int jj = 0; jj < JW; ++jj)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (GELU && 128 * (part + WPR * jj) + 4 * lane + q < K) v[jj][q] = gelu_tab(v[jj][q], s_tab);
+            m = fmax(m, fabs(v[jj][q]));
+        }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if (WPR > 1) {
+        if (lane == 0) s_max[wi] = m;
+        __syncthreads();
+#pragma unroll
+        for (int p2 = 0; p2 < WPR; ++p2) m = fmax(m, s_max[(wi / WPR) * WPR + p2]);
+    }
+    if (!ok) return;
+    const int e = row_exponent(m);
+    if (lane == 0 && part == 0) ex[(int64_t)b * R + r] = e;
+    int8_t *o = out + ((int64_t)b * NS * R + r) * Kp;
+#pragma unroll
+    for (int jj = 0; jj < JW; ++jj) {
+        const int k = 128 * (part + WPR * jj) + 4 * lane;
+        if (k >= Kp) break;
+        uint32_t w[NS];
+        digits4(v[jj], e, w);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) *reinterpret_cast<uint32_t *>(o + (int64_t)s * R * Kp + k) = w[s];
     }
 }
 
@@ -442,16 +453,16 @@ template <typename T, bool GELU = false>
 veda_status split_rows(const T *X, int R, int K, int64_t sr, int64_t sb, int batch, int8_t *out, int32_t *ex,
                        cudaStream_t s)
 {
-    dim3 grid((R + 7) / 8, batch);
     const int Kp = kpad(K);
+    dim3 g8((R + 7) / 8, batch), g4((R + 3) / 4, batch);
     if (Kp <= 128)
-        split_rows_kernel<T, 1, GELU><<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+        split_rows_kernel<T, 1, GELU, 1><<<g8, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
     else if (Kp <= 256)
-        split_rows_kernel<T, 2, GELU><<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+        split_rows_kernel<T, 2, GELU, 1><<<g8, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
     else if (Kp <= 512)
-        split_rows_kernel<T, 4, GELU><<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
-    else if (Kp <= 1024)
-        split_rows_kernel<T, 8, GELU><<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+        split_rows_kernel<T, 4, GELU, 1><<<g8, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+    else if (Kp <= 1024)  // two warps per row: half the registers per thread
+        split_rows_kernel<T, 8, GELU, 2><<<g4, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
     else
         return fail(VEDA_ERR_SHAPE, "ozaki scorer: K=%d > 1024 unsupported", K);
     count_launch();
