@@ -168,8 +168,8 @@ VEDA_API veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int6
  * token order by one TMA box per tile (padded slots zero-filled, reading R4), and each
  * output row stored straight to its token (UnTile).  Bit-identical to
  * veda_tile_permute x3 -> veda_sparse_attn_fwd -> veda_tile_unpermute.
- *   q, k, v : token tensors sharing head_stride / token_stride (elements, multiples of 8,
- *             head_stride != token_stride)
+ *   q, k, v : token tensors sharing head_stride / token_stride (elements, multiples of 8;
+ *             they may be equal only when one of them is unused: one token or one head)
  *   idx [Hh][N_T][k_keep], slot_mask [Hh][N_T][B/32] : as for veda_sparse_attn_fwd
  *   o       : token tensor (o_head_stride, o_token_stride); rows of padded slots are not
  *             written;  lse : [Hh][N_T][B] fp32 (tiled order) or NULL.

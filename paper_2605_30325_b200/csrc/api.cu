@@ -426,8 +426,8 @@ veda_status veda_sparse_attn_fwd_tokens(const uint16_t *q, const uint16_t *k, co
     if (!q || !k || !v || !idx || !slot_mask || !o) return fail(VEDA_ERR_NULL, "sparse_attn_fwd_tokens: NULL pointer");
     if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "sparse_attn_fwd_tokens: d=%d unsupported", d);
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || (head_stride % 8) || (token_stride % 8) ||
-        (o_head_stride % 8) || (o_token_stride % 8) || head_stride == token_stride)
-        return fail(VEDA_ERR_ALIGN, "sparse_attn_fwd_tokens: pointers/strides must be 16-byte aligned and distinct");
+        (o_head_stride % 8) || (o_token_stride % 8))
+        return fail(VEDA_ERR_ALIGN, "sparse_attn_fwd_tokens: pointers/strides must be 16-byte aligned");
     veda_status st = check_arch();
     if (st != VEDA_OK) return st;
     Shape sh;

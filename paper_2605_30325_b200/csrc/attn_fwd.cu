@@ -773,6 +773,16 @@ veda_status launch_sparse_attn_tok(const uint16_t *q, const uint16_t *k, const u
                                    uint16_t *o, int64_t o_hs, int64_t o_ts, float *lse, cudaStream_t s)
 {
     (void)Tp;
+    // a stride that is never used (one token, or one head) may equal the other one; give it
+    // a distinct value so the 5-D tensor maps get a well-ordered dimension set
+    if (hs == ts) {
+        if ((int64_t)T * H * W == 1)
+            ts = hs * Hh;
+        else if (Hh == 1)
+            hs = ts * ((int64_t)T * H * W);
+        else
+            return fail(VEDA_ERR_ALIGN, "sparse_attn_fwd_tokens: head_stride == token_stride");
+    }
 #define VEDA_TOK_ARGS q, k, v, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, idx, mask, kk, scale, o, o_hs, o_ts, lse, s
     if (B == 128 && d == 128) return attn::launch_tok<128, 128>(VEDA_TOK_ARGS);
     if (B == 128 && d == 64) return attn::launch_tok<128, 64>(VEDA_TOK_ARGS);

@@ -538,3 +538,29 @@ def test_scorer_int8_ozaki_vs_fp64_dmma(tmp_path):
     rel = np.abs(a[fin].astype(np.float64) - b[fin]) / np.maximum(1.0, np.abs(b[fin]))
     print(f"ozaki vs dmma: max rel {rel.max():.3e}, identical {np.mean(a[fin] == b[fin]) * 100:.2f} %")
     assert rel.max() < 2e-7
+
+
+@pytest.mark.parametrize("lat,cfg,d", [((1, 1, 1), (4, 4, 8), 128), ((1, 1, 1), (4, 4, 4), 64),
+                                       ((2, 1, 2), (8, 8, 2), 128)])
+def test_degenerate_latents_token_path(V, oracle, lat, cfg, d):
+    """Latents smaller than one tile (a single real token, or a few in one padded tile): the
+    token-layout path keeps exactly the one real key tile (k = N_T = 1) and, with one real
+    token, returns v itself (n = 1 -> output = v); a few tokens match the oracle."""
+    from paper_2605_30325_b200 import synth
+
+    Hh = 2
+    pre = synth.Preset("degenerate", lat, Hh, d, cfg, 0.5)
+    q, k, v = synth.qkv(pre, lat=lat, d=d)
+    w = {n: t.cuda() for n, t in synth.scorer_weights(pre, d=d, random_bias=True).items()}
+    path = V.SparseAttention(lat, [cfg], Hh, d, w, sparsity=0.5)
+    assert path.shape.n_tiles == 1 and path.k == 1
+    o = path(q.cuda(), k.cuda(), v.cuda())
+    torch.cuda.synchronize()
+    assert path.idx.cpu().numpy().tolist() == [[[0]]] * Hh
+    if lat == (1, 1, 1):
+        assert torch.equal(o.cpu(), v)
+    oq, ocnt, omask = oracle.tile_permute(u16(q), lat, [cfg])
+    ok_, _, _ = oracle.tile_permute(u16(k), lat, [cfg])
+    ov, _, _ = oracle.tile_permute(u16(v), lat, [cfg])
+    o_t, _, _ = oracle.tile_permute(u16(o), lat, [cfg])
+    check_attention(oracle, oq, ok_, ov, path.idx.cpu().numpy(), omask, o_t, tag=f"degenerate {lat}")
