@@ -261,6 +261,13 @@ def run_ours(args):
             parts[name] += e[j].elapsed_time(e[j + 1]) / args.steps
     if path.mode == "tokens":  # the token-layout attention stores rows straight to token order
         parts["attn"] += parts.pop("untile")
+    per_step = sorted(e[0].elapsed_time(e[5]) for e in evs)  # each call, first to last step event
+
+    def pct(xs, f):
+        return xs[min(len(xs) - 1, max(0, int(round(f * (len(xs) - 1)))))]
+
+    step_dist = {"p10": round(pct(per_step, 0.1), 3), "median": round(statistics.median(per_step), 3),
+                 "p90": round(pct(per_step, 0.9), 3)}
     ms_step = shard.max_over_ranks(ms_step_local)
     attn_ms = shard.max_over_ranks(parts["attn"])
 
@@ -399,6 +406,7 @@ def run_ours(args):
             "attn_kernel_ms": round(attn_ms, 3),
             "attn_kernel_ms_random_lists": round(rand_attn_ms, 3),
             "step_breakdown_ms": {n: round(t, 3) for n, t in parts.items()},
+            "call_ms_distribution": step_dist,
             "recall_vs_oracle_mask": {"value": round(recall, 4), "chance": round(kk / NT, 4),
                                       "scorer": "random-init (no distilled weights)",
                                       "target_kernel_ms": round(target_ms, 2)},
