@@ -121,3 +121,36 @@ def test_status_strings(lib):
 
     for i, n in enumerate(veda.VEDA_STATUS):
         assert lib.veda_status_str(i).decode() == n
+
+
+def test_token_path_and_host_entry_errors(lib):
+    """Argument validation of the token-layout entry points and the host pipeline: NULL
+    pointers, misaligned strides, k out of range, unsupported layouts and workspace sizing
+    (all checked before any device work)."""
+    from paper_2605_30325_b200 import veda
+
+    fake = ctypes.c_void_p(256)
+    lat = veda.Latent(4, 8, 8)
+    cfg = veda._cfg_array([(4, 4, 4)], 1)
+    st = lib.veda_tile_pool(None, 16384, 64, lat, cfg, 1, 64, fake, None, None, None)
+    assert veda.VEDA_STATUS[st] == "VEDA_ERR_NULL"
+    st = lib.veda_tile_pool(fake, 16384, 63, lat, cfg, 1, 64, fake, None, None, None)
+    assert veda.VEDA_STATUS[st] == "VEDA_ERR_ALIGN"
+    st = lib.veda_tile_pool(fake, 16384, 64, lat, cfg, 1, 96, fake, None, None, None)
+    assert veda.VEDA_STATUS[st] == "VEDA_ERR_SHAPE"
+    st = lib.veda_sparse_attn_fwd_tokens(fake, fake, fake, 16384, 64, lat, cfg, 1, 64, None, fake, 1, 0.0, fake,
+                                         16384, 64, None, None)
+    assert veda.VEDA_STATUS[st] == "VEDA_ERR_NULL"
+    st = lib.veda_sparse_attn_fwd_tokens(fake, fake, fake, 16384, 64, lat, cfg, 1, 64, fake, fake, 1, 0.0,
+                                         ctypes.c_void_p(258), 16384, 64, None, None)
+    assert veda.VEDA_STATUS[st] == "VEDA_ERR_ALIGN"
+    # host pipeline: workspace query validates k and the scorer; layouts must be dense
+    w = veda.Scorer(192, 384, 64, *([fake] * 8))
+    nb = ctypes.c_size_t(0)
+    st = lib.veda_sparse_attention_host_workspace(lat, cfg, 1, 64, 9, ctypes.byref(w), 0, ctypes.byref(nb))
+    assert veda.VEDA_STATUS[st] == "VEDA_ERR_K_RANGE"
+    st = lib.veda_sparse_attention_host_workspace(lat, cfg, 1, 64, 2, ctypes.byref(w), 0, ctypes.byref(nb))
+    assert st == 0 and nb.value > 0
+    st = lib.veda_sparse_attention_host(None, fake, fake, 16384, 64, lat, cfg, 1, 64, 2, ctypes.byref(w), 0, fake,
+                                        fake, nb.value, None)
+    assert veda.VEDA_STATUS[st] == "VEDA_ERR_NULL"
