@@ -13,10 +13,13 @@
  *   - Pointers are DEVICE pointers unless marked "host".  bf16 tensors are passed
  *     as uint16_t bit patterns.  All device pointers must be 16-byte aligned.
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls only
- *     enqueue work and return; they never synchronise, allocate or free device
- *     memory, and keep no pointer after returning.  Host arrays are read during
- *     the call only.  The caller owns every buffer (workspace sizes come from the
- *     *_workspace helpers).
+ *     enqueue work and return; they never allocate or free device memory and keep
+ *     no pointer after returning.  Host arrays are read during the call only.  The
+ *     caller owns every buffer (workspace sizes come from the *_workspace helpers).
+ *     Exceptions, all one-time or bounded: the first scoring call on a device uploads
+ *     a 20 KB constant table (Phi for the GELU) into the library's static device
+ *     memory and synchronises `stream` once; veda_sparse_attention_host creates two
+ *     side streams per device on first use and a few events per call.
  *   - Errors are returned as veda_status; nothing is printed, thrown or aborted.
  *     veda_last_error() gives a thread-local detail string for the last failure.
  *     Faults inside a kernel surface later on the stream as CUDA errors.
