@@ -322,7 +322,7 @@ veda_status veda_tile_score(const uint16_t *q_tiled, const uint16_t *k_tiled, co
     double *ek = reinterpret_cast<double *>(p);
     if ((st = veda_trippool(q_tiled, slot_mask, Hh, n_tiles, B, d, zq, stream)) != VEDA_OK) return st;
     if ((st = veda_trippool(k_tiled, slot_mask, Hh, n_tiles, B, d, zk, stream)) != VEDA_OK) return st;
-    if (scorer_uses_ozaki()) {
+    if (scorer_uses_ozaki() && w->d_in <= 1024 && w->d_hidden <= 1024 && w->d_lat <= 1024) {
         const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
         return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq,
                                   ek, scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),
@@ -356,7 +356,7 @@ veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32
     double *hid = reinterpret_cast<double *>(p); p += align256(rows * w->d_hidden * sizeof(double));
     double *eq = reinterpret_cast<double *>(p); p += align256(rows * w->d_lat * sizeof(double));
     double *ek = reinterpret_cast<double *>(p);
-    if (scorer_uses_ozaki()) {
+    if (scorer_uses_ozaki() && w->d_in <= 1024 && w->d_hidden <= 1024 && w->d_lat <= 1024) {
         const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
         return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq,
                                   ek, scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),

@@ -78,7 +78,8 @@ size_t ozaki_workspace(int Hh, int NT, int din, int dh, int dl);
 veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *cnt, int Hh, int NT, int din, int dh,
                                int dl, const float *const w_q[4], const float *const w_k[4], double *hidden,
                                double *eq, double *ek, float *scores, void *scratch, cudaStream_t s);
-// true unless VEDA_SCORER=dmma (the FP64 tensor-core GEMMs of score.cu) is set at load
+// true unless VEDA_SCORER=dmma (the FP64 tensor-core GEMMs of score.cu) is set at load;
+// scorers with a dimension above 1024 (split_rows holds a row in registers) use DMMA too
 bool scorer_uses_ozaki();
 veda_status launch_sparse_attn_1q(const uint16_t *q, const uint16_t *k, const uint16_t *v, const int32_t *idx,
                                   const uint32_t *mask, int Hh, int NT, int B, int d, int kk, float scale,
