@@ -535,11 +535,17 @@ class SparseAttention:
         mark(5)
         return out
 
-    # scorer launches: INT8 Ozaki (default) = per side 2 x (split rows, split cols, GEMM),
-    # then 2 splits + the score GEMM; VEDA_SCORER=dmma: 2 x 2 phi layers + the score GEMM
-    SCORER_LAUNCHES = 5 if os.environ.get("VEDA_SCORER") == "dmma" else 15
-    # tokens: pool x2, scorer, topk, attn;  tiled: permute x3, pool x2, scorer, topk, attn, unpermute
-    LAUNCHES_PER_CALL = {"tokens": 2 + SCORER_LAUNCHES + 1 + 1, "tiled": 3 + 2 + SCORER_LAUNCHES + 1 + 1 + 1}
+    @property
+    def LAUNCHES_PER_CALL(self):
+        """Kernel launches of one call.  Scorer: INT8 Ozaki (default) = per side 2 x (split
+        rows, split cols, GEMM), then 2 splits + the score GEMM; the FP64 tensor-core path
+        (VEDA_SCORER=dmma, or a scorer dimension above 1024) = 2 x 2 phi layers + scores.
+        tokens: pool x2, scorer, topk, attn;  tiled: permute x3, pool x2, scorer, topk,
+        attn, unpermute."""
+        sc = self.scorer
+        ozaki = (os.environ.get("VEDA_SCORER") != "dmma" and max(sc.d_in, sc.d_hidden, sc.d_lat) <= 1024)
+        n = 15 if ozaki else 5
+        return {"tokens": 2 + n + 1 + 1, "tiled": 3 + 2 + n + 1 + 1 + 1}
 
     def run_host(self, q, k, v, out=None, heads_per_chunk: int = 0):
         """The same call on HOST tensors (veda_sparse_attention_host): q, k, v, out are
