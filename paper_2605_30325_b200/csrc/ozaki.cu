@@ -254,6 +254,92 @@ struct GemmGeo {
 constexpr int EPI_WARPS = 8;
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
+// Epilogue of one 128 x BN output tile, run by the EPI_WARPS epilogue warps: stage the
+// per-column data, wait for the tile's accumulators (done_bar), read this warp's column
+// half from TMEM (releasing TMEM through tfree_bar once all of it is in registers),
+// combine the 5 accumulators exactly, scale, apply the epilogue op and store.
+template <int BN, int EPI>
+__device__ __forceinline__ void epi_tile(const GemmArgs &g, uint32_t tl, int b, int m0, int n0, int cbeg, int cend,
+                                         int row, uint32_t done_bar, uint32_t done_parity, uint32_t tfree_bar,
+                                         int *s_eb, double *s_col)
+{
+    // per-column data of this tile (exponent of B's row, bias / score factor) in smem
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");  // previous tile's readers done
+    for (int c = threadIdx.x - 64; c < BN; c += 32 * EPI_WARPS) {
+        const int n = n0 + c;
+        const bool ok = n < g.N;
+        s_eb[c] = ok ? __ldg(g.eb + (int64_t)b * g.N + n) : 0;
+        if (EPI == EPI_SCORE)
+            s_col[c] = (ok && __ldg(g.cnt + (int64_t)b * g.N + n) != 0) ? 1.0 / g.den : -INFINITY;
+        else
+            s_col[c] = ok ? (double)__ldg(g.bias + (int64_t)b * g.N + n) : 0.0;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+    const int m = m0 + row;
+    const bool mok = m < g.M;
+    const int ea = mok ? __ldg(g.ea + (int64_t)b * g.M + m) : 0;
+    mbar_wait(done_bar, done_parity);
+    tc_fence_after();
+    const int64_t orow = ((int64_t)b * g.M + m) * g.N;
+#pragma unroll 1
+    for (int c0 = cbeg; c0 < cend; c0 += 16) {
+        uint32_t acc[NS][16];
+#pragma unroll
+        for (int u = 0; u < NS; ++u) tmem_ld16(tl + (uint32_t)(u * BN + c0), acc[u]);
+        tmem_wait_ld();
+        if (c0 + 16 >= cend) {  // this warp's accumulator columns are in registers
+            tc_fence_before();
+            mbar_arrive(tfree_bar);
+        }
+        if (!mok) continue;
+        // vector stores only when the whole 16-column run is in range and aligned
+        const bool full = n0 + c0 + 16 <= g.N && (g.N % 4) == 0;
+        double out[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            // sum_u acc_u 2^-(7u+12) = 2^-40 * sum_u acc_u 2^(7(4-u)): |acc_u| < 2^24, so
+            // the weighted sum is an exact int64 below 2^53 and converts to fp64 exactly
+            int64_t iv = 0;
+#pragma unroll
+            for (int u = 0; u < NS; ++u) iv += (int64_t)(int32_t)acc[u][i] << (7 * (NS - 1 - u));
+            const int sc = ea + s_eb[c0 + i] - (7 * (NS - 1) + 12) + 1023;  // biased exponent
+            const double v = (double)iv * __longlong_as_double((long long)sc << 52);
+            if (EPI == EPI_SCORE) {
+                const double f = s_col[c0 + i];  // 1/sqrt(d'), or -inf for an empty key tile
+                out[i] = (f == -INFINITY) ? -INFINITY : v * f;
+            } else if (EPI == EPI_GELU) {
+                out[i] = gelu_tab_g(v + s_col[c0 + i]);  // hidden = GELU(z W1 + b1)
+            } else {
+                out[i] = v + s_col[c0 + i];  // + bias
+            }
+        }
+        if (EPI == EPI_SCORE) {
+            float *dst = static_cast<float *>(g.C) + orow + n0 + c0;
+            if (full) {
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                    *reinterpret_cast<float4 *>(dst + i) =
+                        make_float4((float)out[i], (float)out[i + 1], (float)out[i + 2], (float)out[i + 3]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (n0 + c0 + i < g.N) dst[i] = (float)out[i];
+            }
+        } else {
+            double *dst = static_cast<double *>(g.C) + orow + n0 + c0;
+            if (full) {
+#pragma unroll
+                for (int i = 0; i < 16; i += 2)
+                    *reinterpret_cast<double2 *>(dst + i) = make_double2(out[i], out[i + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (n0 + c0 + i < g.N) dst[i] = out[i];
+            }
+        }
+    }
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                   const __grid_constant__ CUtensorMap tmB,
@@ -355,81 +441,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
             int b, m0, n0;
             tile_coords(t, b, m0, n0);
-            // per-column data of this tile (exponent of B's row, bias / score factor) in smem
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");  // previous tile's readers done
-            for (int c = threadIdx.x - 64; c < BN; c += 32 * EPI_WARPS) {
-                const int n = n0 + c;
-                const bool ok = n < g.N;
-                s_eb[c] = ok ? __ldg(g.eb + (int64_t)b * g.N + n) : 0;
-                if (EPI == EPI_SCORE)
-                    s_col[c] = (ok && __ldg(g.cnt + (int64_t)b * g.N + n) != 0) ? 1.0 / g.den : -INFINITY;
-                else
-                    s_col[c] = ok ? (double)__ldg(g.bias + (int64_t)b * g.N + n) : 0.0;
-            }
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
-            const int m = m0 + row;
-            const bool mok = m < g.M;
-            const int ea = mok ? __ldg(g.ea + (int64_t)b * g.M + m) : 0;
-            mbar_wait(OZ_DONE, (uint32_t)nt & 1u);
-            tc_fence_after();
-            const int64_t orow = ((int64_t)b * g.M + m) * g.N;
-#pragma unroll 1
-            for (int c0 = cbeg; c0 < cend; c0 += 16) {
-                uint32_t acc[NS][16];
-#pragma unroll
-                for (int u = 0; u < NS; ++u) tmem_ld16(tl + (uint32_t)(u * BN + c0), acc[u]);
-                tmem_wait_ld();
-                if (c0 + 16 >= cend) {  // this warp's accumulator columns are in registers
-                    tc_fence_before();
-                    mbar_arrive(OZ_TFREE);
-                }
-                if (!mok) continue;
-                // vector stores only when the whole 16-column run is in range and aligned
-                const bool full = n0 + c0 + 16 <= g.N && (g.N % 4) == 0;
-                double out[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    // sum_u acc_u 2^-(7u+12) = 2^-40 * sum_u acc_u 2^(7(4-u)): |acc_u| < 2^24, so
-                    // the weighted sum is an exact int64 below 2^53 and converts to fp64 exactly
-                    int64_t iv = 0;
-#pragma unroll
-                    for (int u = 0; u < NS; ++u) iv += (int64_t)(int32_t)acc[u][i] << (7 * (NS - 1 - u));
-                    const int sc = ea + s_eb[c0 + i] - (7 * (NS - 1) + 12) + 1023;  // biased exponent
-                    const double v = (double)iv * __longlong_as_double((long long)sc << 52);
-                    if (EPI == EPI_SCORE) {
-                        const double f = s_col[c0 + i];  // 1/sqrt(d'), or -inf for an empty key tile
-                        out[i] = (f == -INFINITY) ? -INFINITY : v * f;
-                    } else if (EPI == EPI_GELU) {
-                        out[i] = gelu_tab_g(v + s_col[c0 + i]);  // hidden = GELU(z W1 + b1)
-                    } else {
-                        out[i] = v + s_col[c0 + i];  // + bias
-                    }
-                }
-                if (EPI == EPI_SCORE) {
-                    float *dst = static_cast<float *>(g.C) + orow + n0 + c0;
-                    if (full) {
-#pragma unroll
-                        for (int i = 0; i < 16; i += 4)
-                            *reinterpret_cast<float4 *>(dst + i) =
-                                make_float4((float)out[i], (float)out[i + 1], (float)out[i + 2], (float)out[i + 3]);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            if (n0 + c0 + i < g.N) dst[i] = (float)out[i];
-                    }
-                } else {
-                    double *dst = static_cast<double *>(g.C) + orow + n0 + c0;
-                    if (full) {
-#pragma unroll
-                        for (int i = 0; i < 16; i += 2)
-                            *reinterpret_cast<double2 *>(dst + i) = make_double2(out[i], out[i + 1]);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            if (n0 + c0 + i < g.N) dst[i] = out[i];
-                    }
-                }
-            }
+            epi_tile<BN, EPI>(g, tl, b, m0, n0, cbeg, cend, row, OZ_DONE, (uint32_t)nt & 1u, OZ_TFREE, s_eb, s_col);
         }
     }
     tc_fence_before();
