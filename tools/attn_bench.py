@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--regime", default="path")
     ap.add_argument("--workload", default="waver12b")
+    ap.add_argument("--tokens", action="store_true", help="time the token-layout kernel (the path's) instead")
     a = ap.parse_args()
     veda.load()
     pre = synth.PRESETS[a.workload]
@@ -35,19 +36,24 @@ def main():
         kk = NT
     else:
         idx = path.idx
-    out = torch.empty_like(path.ot)
-    veda.sparse_attn_fwd(path.qt, path.kt, path.vt, idx, path.mask, out=out)
+    if a.tokens:
+        out = torch.empty_like(q)
+        run = lambda: veda.sparse_attn_fwd_tokens(q, k, v, pre.lat, [pre.cfg], idx, path.mask, out=out)
+    else:
+        out = torch.empty_like(path.ot)
+        run = lambda: veda.sparse_attn_fwd(path.qt, path.kt, path.vt, idx, path.mask, out=out)
+    run()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(a.reps):
-        veda.sparse_attn_fwd(path.qt, path.kt, path.vt, idx, path.mask, out=out)
+        run()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.reps
     flops = 4.0 * B * B * pre.d * kk * NT * len(heads)
-    ref = veda.sparse_attn_fwd(path.qt, path.kt, path.vt, idx, path.mask)
     print(f"{os.environ.get('VEDA_LIB', 'libveda.so').split('/')[-1]:28s} {a.regime:6s} heads={a.heads} "
+          f"{'tokens' if a.tokens else 'tiled'} "
           f"{ms:8.3f} ms  {flops / ms / 1e9:7.1f} TFLOP/s", flush=True)
     return out
 
