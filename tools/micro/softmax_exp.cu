@@ -88,6 +88,78 @@ __global__ void kern(const float *in, uint32_t *out, long long *cyc, int reps)
     if ((threadIdx.x & 31) == 0) cyc[blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32] = t1 - t0;
 }
 
+// Interference probe: warps 0-3 (one per SMSP) run the exp phase; warps 4-7 (one more per
+// SMSP) run an interference loop until the exp warps finish: MODE 1 = mbarrier try_wait on
+// a phase that never completes (an idle waiter), MODE 2 = FMNMX3 chains (another warp's
+// row-max phase), MODE 3 = the exp phase itself (MUFU contention).
+template <int MODE>
+__global__ void interfere(const float *in, uint32_t *out, long long *cyc, int reps)
+{
+    __shared__ unsigned long long bar;
+    __shared__ volatile int done;
+    if (threadIdx.x == 0) {
+        done = 0;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bar)));
+    }
+    __syncthreads();
+    const int w = threadIdx.x >> 5;
+    if (w >= 4) {
+        float a = in[threadIdx.x & 1023], b = a + 1.f, c = a - 1.f;
+        uint32_t spins = 0;
+        while (!done) {
+            if (MODE == 1) {
+                uint32_t ok;
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                             "selp.u32 %0, 1, 0, p;\n\t}"
+                             : "=r"(ok) : "r"((uint32_t)__cvta_generic_to_shared(&bar)) : "memory");
+                spins += ok;
+            } else if (MODE == 2) {
+#pragma unroll
+                for (int i = 0; i < 64; ++i) {
+                    float d;
+                    asm volatile("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+                    a = b; b = c; c = d;
+                }
+            } else if (MODE == 3) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) { a = ex2f(a * 0.5f); b = ex2f(b * 0.5f); }
+            }
+        }
+        out[blockIdx.x * blockDim.x + threadIdx.x] = __float_as_uint(a + b + c) + spins;
+        return;
+    }
+    float s[128];
+    for (int i = 0; i < 128; ++i) s[i] = in[(threadIdx.x * 7 + i) & 1023] * 0.01f;
+    uint32_t acc = 0;
+    float tot = 0.f;
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+        const float sl2 = 0.127f + r * 1e-9f, mu = 3.0f;
+        float ps[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) {
+            uint32_t pk[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int e = c2 * 64 + 2 * i;
+                float x0, x1;
+                ffma2(x0, x1, s[e], s[e + 1], sl2, -mu);
+                const float a = ex2f(x0), b = ex2f(x1);
+                fadd2(ps[(i & 1) * 2], ps[(i & 1) * 2 + 1], a, b);
+                pk[i] = pack(a, b);
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc ^= pk[i];
+        }
+        tot += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+    }
+    const long long t1 = clock64();
+    asm volatile("bar.sync 1, 128;");
+    if (threadIdx.x == 0) done = 1;
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc ^ __float_as_uint(tot);
+    if ((threadIdx.x & 31) == 0) cyc[blockIdx.x * 4 + w] = t1 - t0;
+}
+
 int main()
 {
     int sms;
@@ -114,6 +186,18 @@ int main()
             printf("warps/SMSP=%d emu=%d: %.0f clk per 128-element exp phase per warp (%.0f per SMSP-tile)\n", wps,
                    emu, m / reps, m / reps / wps);
         }
+    }
+    for (int mode = 0; mode <= 3; ++mode) {
+        if (mode == 0) interfere<0><<<sms, 256>>>(in, out, cyc, reps);
+        if (mode == 1) interfere<1><<<sms, 256>>>(in, out, cyc, reps);
+        if (mode == 2) interfere<2><<<sms, 256>>>(in, out, cyc, reps);
+        if (mode == 3) interfere<3><<<sms, 256>>>(in, out, cyc, reps);
+        cudaDeviceSynchronize();
+        long long h[4];
+        cudaMemcpy(h, cyc, 4 * 8, cudaMemcpyDeviceToHost);
+        const double m = (h[0] + h[1] + h[2] + h[3]) / 4.0 / reps;
+        const char *names[] = {"none", "mbarrier try_wait spinner", "FMNMX3 chains", "MUFU ex2 loop"};
+        printf("exp phase with one interfering warp per SMSP (%s): %.0f clk\n", names[mode], m);
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
