@@ -8,9 +8,14 @@
 // B200 design:
 //  * persistent, one CTA per SM, 384 threads = 3 warpgroups:
 //      warp 0      TMA producer: Q tiles and the kept K/V tiles -> SMEM ring (SWIZZLE_128B)
-//      warp 1      MMA issuer (one thread): tcgen05.mma, S = Q K^T (SS) and O += P V (TS)
-//      warps 2-3   idle (warpgroup 0 gives its registers away with setmaxnreg)
+//      warp 1      MMA issuer (warp-uniform, one elected lane): tcgen05.mma,
+//                  S = Q K^T (SS) and O += P V (TS)
+//      warps 2-3   ring-stage release for slot 0 / slot 1 (warpgroup 0 gives its spare
+//                  registers to the softmax warpgroups with setmaxnreg)
 //      warps 4-11  two softmax warpgroups ("slots"), one query tile each, one row per thread
+//  * two addressing modes: tiled tensors [Hh][N_T][B][d] (2-D TMA boxes, tiled output), or
+//    TOK: tiles gathered from token order by one 5-D TMA box each and output rows stored
+//    straight to token order (no tiled copies; the path's mode)
 //  * each slot owns 256 TMEM columns: S (fp32, 128 cols; P aliases its first B/2 columns
 //    as packed bf16) and O (fp32, D cols).  The two slots work on different query
 //    tiles with independent kept lists, so one slot's softmax overlaps the other's MMAs.
