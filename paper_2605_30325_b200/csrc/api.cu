@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libveda (include/veda.h): argument validation, shape helpers,
 // workspace carving and kernel dispatch.  All device work is in permute.cu, score.cu,
-// topk.cu and attn_fwd.cu; nothing here touches data.
+// ozaki.cu, topk.cu, attn_fwd.cu (+ attn_fwd_1q.cu), target.cu and search.cu, and the
+// host-buffer pipeline in pipeline.cu; nothing here touches data.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>

@@ -6,8 +6,11 @@
 //   S_pred, Eq. 6 (Alg. 2): S_ij = e_q,i . e_k,j / sqrt(d').
 //
 // Precision (R17): the kept index lists must match the fp64 oracle except at
-// near-ties < 1e-5, so every reduction here accumulates in fp64 on the FP64 pipe
-// (fp32 x fp32 products are exact in fp64); scores are rounded once to fp32.
+// near-ties < 1e-5, so every reduction here accumulates in fp64 (fp32 x fp32 products are
+// exact in fp64); scores are rounded once to fp32.  This file holds the pooling kernels
+// (tiled and token-layout) and the FP64-tensor-core (DMMA) GEMMs of phi / S_pred, used by
+// veda_project / veda_pair_scores and by veda_tile_score when VEDA_SCORER=dmma; the
+// default scorer GEMMs run on the INT8 tensor cores (ozaki.cu).
 #include <cmath>
 #include <cstdlib>
 
