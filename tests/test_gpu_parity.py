@@ -450,6 +450,22 @@ def test_alt_schedule_1q_parity():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+def test_alt_schedule_hs_parity():
+    """The half-step schedule (sparse_attn_fwd_hs_kernel in csrc/attn_fwd.cu, VEDA_ATTN=hs)
+    passes the attention parity tests of both layouts, in a fresh process."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, VEDA_ATTN="hs")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_parity.py"),
+                        "-k", "test_attention_vs_oracle or test_dense_k_equals_nt or test_random_lists_and_small_k or "
+                        "test_end_to_end_path_object or tokens_equals_tiled or full_size_sampled or degenerate_latents"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("NT,k", [(1, 1), (7, 3), (33, 32), (128, 5), (336, 34), (700, 36), (1920, 96),
                                   (2048, 2048), (2049, 100), (4880, 96)])
 def test_topk_sizes_and_ties_bit_exact(V, oracle, NT, k):
