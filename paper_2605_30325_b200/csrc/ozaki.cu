@@ -78,20 +78,24 @@ __device__ __forceinline__ void digits4(const double (&x)[4], int e, uint32_t (&
 
 // GELU(x) = x Phi(x) (erf form, reading R8) in fp64 without the libdevice erf (which costs
 // ~70 FP64 instructions and made the layer-2 split FP64-bound): Phi on [-8, 8] from a
-// table of degree-9 Taylor polynomials around the centres of 256 intervals of width 1/16
-// (truncation error < 1e-16 relative; coefficients from Phi(c) = erfc(-c/sqrt2)/2 and
+// table of degree-5 Taylor polynomials around the centres of 768 intervals of width 1/48
+// (|error| <= 3.5e-15 absolute over [-8, 8], a few ulp; three double2 loads per value -- the
+// split is bound by these shared-memory reads; coefficients from Phi(c) = erfc(-c/sqrt2)/2 and
 // Phi^(n+1)(c) = (-1)^n He_n(c) phi(c), built once on the host); |x| >= 8: Phi = 0 or 1
 // (error < 7e-16).
-constexpr int PHI_N = 256, PHI_DEG = 9;  // PHI_DEG + 1 coefficients, read as double2 pairs
+constexpr int PHI_N = 768, PHI_DEG = 5;  // PHI_DEG + 1 coefficients, read as double2 pairs
+constexpr double PHI_SCALE = 48.0;        // intervals per unit of x: PHI_N = 16 * PHI_SCALE
+constexpr double PHI_W = 1.0 / 48.0;      // interval width (rounded); centre i: fma(i + 0.5, PHI_W, -8), host and device
+static_assert(PHI_N == 16 * 48 && (PHI_DEG + 1) % 2 == 0, "Phi table layout");
 __device__ __align__(16) double g_phi_tab[PHI_N][PHI_DEG + 1];
 
 __device__ __forceinline__ double gelu_tab(double x, const double2 (*tab)[(PHI_DEG + 1) / 2])
 {
     if (x >= 8.0) return x;
     if (x <= -8.0) return 0.0;
-    int i = (int)((x + 8.0) * 16.0);
+    int i = (int)((x + 8.0) * PHI_SCALE);
     if (i > PHI_N - 1) i = PHI_N - 1;
-    const double h = x - (-8.0 + (i + 0.5) / 16.0);
+    const double h = x - fma((double)i + 0.5, PHI_W, -8.0);  // no fp64 division
     const double2 *c = tab[i];
     double2 q = c[(PHI_DEG + 1) / 2 - 1];
     double p = fma(q.y, h, q.x);
@@ -115,61 +119,69 @@ __device__ __forceinline__ double gelu_tab_g(double x)
 // pre-activation and the digits are those of GELU(x) (erf form, reading R8).
 template <typename T, int J, bool GELU, int WPR>
 __global__ void __launch_bounds__(256) split_rows_kernel(const T *__restrict__ X, int R, int K, int64_t sr,
-                                                         int64_t sb, int Kp, int8_t *__restrict__ out,
+                                                         int64_t sb, int Kp, int batch, int8_t *__restrict__ out,
                                                          int32_t *__restrict__ ex)
 {
     // WPR warps share a row (each holds J/WPR of its 128-column chunks, fewer registers ->
     // more resident warps); the row maximum is combined through shared memory.
-    // GELU: the Phi table is staged in shared memory once per block.
+    // GELU: the Phi table is staged in shared memory once per block, and the block loops
+    // over row groups (grid = resident blocks) so that staging is paid once per block.
     constexpr int JW = J / WPR, RPB = 8 / WPR;
     __shared__ double2 s_tab[GELU ? PHI_N : 1][(PHI_DEG + 1) / 2];
-    __shared__ double s_max[8];
+    __shared__ double s_max[2][8];  // by iteration parity: one __syncthreads per iteration suffices
     if (GELU) {
         const double2 *g = reinterpret_cast<const double2 *>(&g_phi_tab[0][0]);
         double2 *d = &s_tab[0][0];
         for (int i = threadIdx.x; i < PHI_N * (PHI_DEG + 1) / 2; i += 256) d[i] = g[i];
         __syncthreads();
     }
-    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, part = wi % WPR, b = blockIdx.y;
-    const int r = blockIdx.x * RPB + wi / WPR;
-    const bool ok = r < R;
-    const T *x = X + b * sb + (int64_t)(ok ? r : 0) * sr;
-    double v[JW][4];
-    double m = 0.0;
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, part = wi % WPR;
+    const int nbx = (R + RPB - 1) / RPB;
+    // without GELU: one row group per block (grid nbx x batch), the loop runs once
+    const int nblk = GELU ? nbx * batch : 1;
+    int it = 0;
+    for (int blk = GELU ? (int)blockIdx.x : 0; blk < nblk; blk += GELU ? (int)gridDim.x : 1, ++it) {
+        const int b = GELU ? blk / nbx : (int)blockIdx.y;
+        const int r = (GELU ? blk - b * nbx : (int)blockIdx.x) * RPB + wi / WPR;
+        const bool ok = r < R;
+        const T *x = X + b * sb + (int64_t)(ok ? r : 0) * sr;
+        double v[JW][4];
+        double m = 0.0;
 #pragma unroll
-    for (int jj = 0; jj < JW; ++jj)  // all loads first (K and the row start are multiples of 4)
+        for (int jj = 0; jj < JW; ++jj)  // all loads first (K and the row start are multiples of 4)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int k = 128 * (part + WPR * jj) + 4 * lane + q;
-            v[jj][q] = (ok && k < K) ? (double)__ldg(x + k) : 0.0;
+            for (int q = 0; q < 4; ++q) {
+                const int k = 128 * (part + WPR * jj) + 4 * lane + q;
+                v[jj][q] = (ok && k < K) ? (double)__ldg(x + k) : 0.0;
+            }
+#pragma unroll
+        for (int jj = 0; jj < JW; ++jj)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (GELU && 128 * (part + WPR * jj) + 4 * lane + q < K) v[jj][q] = gelu_tab(v[jj][q], s_tab);
+                m = fmax(m, fabs(v[jj][q]));
+            }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (WPR > 1) {
+            if (lane == 0) s_max[it & 1][wi] = m;
+            __syncthreads();
+#pragma unroll
+            for (int p2 = 0; p2 < WPR; ++p2) m = fmax(m, s_max[it & 1][(wi / WPR) * WPR + p2]);
         }
+        if (!ok) continue;
+        const int e = row_exponent(m);
+        if (lane == 0 && part == 0) ex[(int64_t)b * R + r] = e;
+        int8_t *o = out + ((int64_t)b * NS * R + r) * Kp;
 #pragma unroll
-    for (int jj = 0; jj < JW; ++jj)
+        for (int jj = 0; jj < JW; ++jj) {
+            const int k = 128 * (part + WPR * jj) + 4 * lane;
+            if (k >= Kp) break;
+            uint32_t w[NS];
+            digits4(v[jj], e, w);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (GELU && 128 * (part + WPR * jj) + 4 * lane + q < K) v[jj][q] = gelu_tab(v[jj][q], s_tab);
-            m = fmax(m, fabs(v[jj][q]));
+            for (int s = 0; s < NS; ++s) *reinterpret_cast<uint32_t *>(o + (int64_t)s * R * Kp + k) = w[s];
         }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-    if (WPR > 1) {
-        if (lane == 0) s_max[wi] = m;
-        __syncthreads();
-#pragma unroll
-        for (int p2 = 0; p2 < WPR; ++p2) m = fmax(m, s_max[(wi / WPR) * WPR + p2]);
-    }
-    if (!ok) return;
-    const int e = row_exponent(m);
-    if (lane == 0 && part == 0) ex[(int64_t)b * R + r] = e;
-    int8_t *o = out + ((int64_t)b * NS * R + r) * Kp;
-#pragma unroll
-    for (int jj = 0; jj < JW; ++jj) {
-        const int k = 128 * (part + WPR * jj) + 4 * lane;
-        if (k >= Kp) break;
-        uint32_t w[NS];
-        digits4(v[jj], e, w);
-#pragma unroll
-        for (int s = 0; s < NS; ++s) *reinterpret_cast<uint32_t *>(o + (int64_t)s * R * Kp + k) = w[s];
     }
 }
 
@@ -466,15 +478,27 @@ veda_status split_rows(const T *X, int R, int K, int64_t sr, int64_t sb, int bat
                        cudaStream_t s)
 {
     const int Kp = kpad(K);
-    dim3 g8((R + 7) / 8, batch), g4((R + 3) / 4, batch);
+    // one block per row group, or (GELU) as many as are resident, each looping over groups
+    auto go = [&](auto kern, int rpb) {
+        const int nbx = (R + rpb - 1) / rpb, total = nbx * batch;
+        dim3 grid(nbx, batch);
+        if (GELU) {
+            static int per_sm = 0;  // per instantiation of split_rows<T, GELU>
+            if (per_sm == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess)
+                per_sm = 1;
+            if (per_sm < 1) per_sm = 1;
+            grid = dim3(std::min(total, per_sm * num_sms()), 1);
+        }
+        kern<<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, batch, out, ex);
+    };
     if (Kp <= 128)
-        split_rows_kernel<T, 1, GELU, 1><<<g8, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+        go(split_rows_kernel<T, 1, GELU, 1>, 8);
     else if (Kp <= 256)
-        split_rows_kernel<T, 2, GELU, 1><<<g8, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+        go(split_rows_kernel<T, 2, GELU, 1>, 8);
     else if (Kp <= 512)
-        split_rows_kernel<T, 4, GELU, 1><<<g8, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+        go(split_rows_kernel<T, 4, GELU, 1>, 8);
     else if (Kp <= 1024)  // two warps per row: half the registers per thread
-        split_rows_kernel<T, 8, GELU, 2><<<g4, 256, 0, s>>>(X, R, K, sr, sb, Kp, out, ex);
+        go(split_rows_kernel<T, 8, GELU, 2>, 4);
     else
         return fail(VEDA_ERR_SHAPE, "ozaki scorer: K=%d > 1024 unsupported", K);
     count_launch();
@@ -554,7 +578,7 @@ static veda_status phi_table_ready(cudaStream_t s)
     static double tab[oz::PHI_N][oz::PHI_DEG + 1];
     const double inv_sqrt2pi = 0.39894228040143267794;
     for (int i = 0; i < oz::PHI_N; ++i) {
-        const double c = -8.0 + (i + 0.5) / 16.0;
+        const double c = std::fma((double)i + 0.5, oz::PHI_W, -8.0);  // the device's centre, bit for bit
         const double phi = inv_sqrt2pi * std::exp(-0.5 * c * c);
         tab[i][0] = 0.5 * std::erfc(-c / std::sqrt(2.0));
         // He_0 = 1, He_1 = c, He_{n+1} = c He_n - n He_{n-1};  coefficient of h^(n+1): (-1)^n He_n phi / (n+1)!
