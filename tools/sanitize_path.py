@@ -39,6 +39,18 @@ def main():
         torch.cuda.synchronize()
         assert torch.equal(oh.view(torch.int16), o.cpu().view(torch.int16))
         print(f"{name}: ok (k={path.k}, n_tiles={path.shape.n_tiles})", flush=True)
+    # scorer at a size where the GELU split's blocks loop over several row groups (R = 2 x 1000
+    # rows, 500 row groups > the resident grid)
+    pre = synth.Preset("scorer", (8, 16, 16), 2, 128, (4, 4, 8), 0.5)
+    w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, d=128, random_bias=True).items()}
+    NT = 1000
+    g = torch.Generator().manual_seed(5)
+    zq, zk = (torch.randn(2, NT, 3 * 128, generator=g).to(dev) for _ in range(2))
+    cnt = torch.full((2, NT), 128, dtype=torch.int32, device=dev)
+    s1 = veda.tile_score_pooled(zq, zk, cnt, veda.make_scorer(w))
+    torch.cuda.synchronize()
+    assert torch.isfinite(s1).all()
+    print(f"scorer NT={NT}: ok", flush=True)
     for NT, kk in ((300, 17), (2100, 50)):  # warp and CTA top-k kernels
         s = torch.randn(2, NT, NT, device=dev)
         veda.select_topk(s, kk)
