@@ -645,6 +645,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // ends.  Static MMA order per half-step g: QK(s, g+1) for both slots, then PV(s, g) for both
 // slots; ring stages are committed free by the MMA thread (K after its 2nd half's QK, V
 // after its 2nd half's PV).  Producer order: K(s,0); then per tile t: V(s,t), K(s,t+1).
+// The half-step softmax holds 64 scores per thread (not 128), so registers move from the
+// softmax warpgroups to the control warpgroup, whose MMA thread keeps per-slot state for
+// both slots (104 + 2 x 200 = 504 per thread slot, as 72 + 2 x 216).
+constexpr int REGS_CTRL_HS = 104, REGS_SOFTMAX_HS = 200;
+
 template <int B, int D>
 struct GeoHS {
     static constexpr int HB = B / 2;                  // keys per half
@@ -733,7 +738,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     if (warp < 4) {
 #ifndef VEDA_NO_SETMAXNREG
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS_CTRL));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS_CTRL_HS));
 #endif
         if (warp == 0) {
             // ============================ TMA producer ============================
@@ -805,9 +810,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             };
             // S(half) = Q K_half^T: keys [half*HB, half*HB + HB) of the tile in stage st
             auto issue_qk = [&](int s, uint32_t st, int half) {
-                const uint64_t ad0 = sdesc_sw128(sQ + s * G::Q_BYTES, 16, 1024);
-                const uint64_t bd0 = sdesc_sw128(sRing + st * G::TILE_BYTES + (uint32_t)(half * HB * 128), 16, 1024);
-                const uint32_t tS = tbase + s * 256 + G::T_S;
+                // shfl from lane 0: lets ptxas treat the operands as warp-uniform (UR registers,
+                // MMAs back to back) instead of converting them per MMA
+                const uint64_t ad0 = __shfl_sync(0xFFFFFFFFu, sdesc_sw128(sQ + s * G::Q_BYTES, 16, 1024), 0);
+                const uint64_t bd0 = __shfl_sync(
+                    0xFFFFFFFFu, sdesc_sw128(sRing + st * G::TILE_BYTES + (uint32_t)(half * HB * 128), 16, 1024), 0);
+                const uint32_t tS = __shfl_sync(0xFFFFFFFFu, tbase + s * 256 + G::T_S, 0);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const uint64_t ao = (uint64_t)(((kk >> 2) * G::QCHUNK + (kk & 3) * 32) >> 4);
@@ -817,13 +825,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             };
             // O += P(half) V_half: P from TMEM buffer half&1... (global half parity), V keys of the half
             auto issue_pv = [&](int s, uint32_t st, int half, int pbuf, bool first) {
-                const uint64_t vd0 = sdesc_sw128(sRing + st * G::TILE_BYTES, G::KCHUNK, 1024);
-                const uint32_t tP = tbase + s * 256 + (pbuf ? G::T_P1 : G::T_P0), tO = tbase + s * 256 + G::T_O;
+                const uint64_t vd0 = __shfl_sync(
+                    0xFFFFFFFFu,
+                    sdesc_sw128(sRing + st * G::TILE_BYTES + (uint32_t)(half * HB * 128), G::KCHUNK, 1024), 0);
+                const uint32_t tP = __shfl_sync(0xFFFFFFFFu, tbase + s * 256 + (pbuf ? G::T_P1 : G::T_P0), 0);
+                const uint32_t tO = __shfl_sync(0xFFFFFFFFu, tbase + s * 256 + G::T_O, 0);
 #pragma unroll
-                for (int kk = 0; kk < HB / 16; ++kk) {
-                    const int kg = half * (HB / 16) + kk;  // 16-key step inside the tile
-                    mma_ts_w(tO, tP + kk * 8, vd0 + (uint64_t)((kg * 2048) >> 4), idesc_pv, (!first || kk > 0) ? 1u : 0u);
-                }
+                for (int kk = 0; kk < HB / 16; ++kk)  // 16 keys = 16 rows of 128 B of the V half
+                    mma_ts_w(tO, tP + kk * 8, vd0 + (uint64_t)((kk * 2048) >> 4), idesc_pv, (!first || kk > 0) ? 1u : 0u);
             };
             uint32_t kst[NSLOT] = {0, 0}, kph[NSLOT] = {0, 0}, vst[NSLOT] = {0, 0}, vph[NSLOT] = {0, 0};
             for (int r = 0; r < rounds; ++r) {
@@ -904,7 +913,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else {
 #ifndef VEDA_NO_SETMAXNREG
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_SOFTMAX));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_SOFTMAX_HS));
 #endif
         // ============================ softmax warpgroups ============================
         const int slot = (warp - 4) >> 2;
