@@ -450,15 +450,18 @@ def test_alt_schedule_1q_parity():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-def test_alt_schedule_hs_parity():
-    """The half-step schedule (sparse_attn_fwd_hs_kernel in csrc/attn_fwd.cu, VEDA_ATTN=hs)
-    passes the attention parity tests of both layouts, in a fresh process."""
+@pytest.mark.parametrize("schedule", ["hs", "ps"])
+def test_alt_schedule_parity(schedule):
+    """The half-step schedule (sparse_attn_fwd_hs_kernel, VEDA_ATTN=hs) and the P-in-shared-
+    memory schedule (sparse_attn_fwd_ps_kernel, VEDA_ATTN=ps; B = d = 128 launches, the
+    others fall back to the default kernel) pass the attention parity tests of both
+    layouts, in a fresh process."""
     import os
     import subprocess
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
-    env = dict(os.environ, VEDA_ATTN="hs")
+    env = dict(os.environ, VEDA_ATTN=schedule)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_parity.py"),
                         "-k", "test_attention_vs_oracle or test_dense_k_equals_nt or test_random_lists_and_small_k or "
                         "test_end_to_end_path_object or tokens_equals_tiled or full_size_sampled or degenerate_latents"],
