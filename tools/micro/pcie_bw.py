@@ -1,0 +1,17 @@
+"""Pinned-memory PCIe bandwidth at the e2e transfer sizes of the Waver call (4.05 GB H2D, 1.35 GB D2H)."""
+import torch, time
+n = 4047667200 // 2
+h = torch.empty(n, dtype=torch.bfloat16).pin_memory()
+d = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+o = torch.empty(1349222400 // 2, dtype=torch.bfloat16, device="cuda")
+oh = torch.empty(o.numel(), dtype=torch.bfloat16).pin_memory()
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+for it in range(3):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(); e0.record()
+    d.copy_(h, non_blocking=True); e1.record(); torch.cuda.synchronize()
+    t = e0.elapsed_time(e1)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(); oh.copy_(o, non_blocking=True); e3.record(); torch.cuda.synchronize()
+    t2 = e2.elapsed_time(e3)
+    print(f"H2D 4.05 GB: {t:.1f} ms ({4.0477/t*1e3:.1f} GB/s); D2H 1.35 GB: {t2:.1f} ms ({1.3492/t2*1e3:.1f} GB/s)")
