@@ -122,6 +122,23 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const float *__restric
 // ballots over i -- the same contract as topk_kernel above, without smem or CTA syncs.
 constexpr int TKW_WARPS = 8;
 
+// #{i : key[i] >= c} for this lane (c >= 1, or c = 0 meaning "none": see the caller): key +
+// (2^32 - c) carries out iff key >= c, so each key costs one add-with-carry-out and one
+// add of the carry (two instructions) instead of compare + select + add, and four
+// independent accumulators keep the adds off a single dependency chain.
+template <int C>
+__device__ __forceinline__ uint32_t count_ge(const uint32_t (&key)[C], uint32_t c)
+{
+    const uint32_t negc = 0u - c;
+    uint32_t n[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0; i < C; ++i)
+        asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, 0;\n\t}"
+            : "+r"(n[i & 3])
+            : "r"(key[i]), "r"(negc));
+    return (n[0] + n[1]) + (n[2] + n[3]);
+}
+
 template <int C>
 __global__ void __launch_bounds__(TKW_WARPS * 32) topk_warp_kernel(const float *__restrict__ S, int rows, int NT,
                                                                    int k, int32_t *__restrict__ idx)
@@ -141,19 +158,15 @@ __global__ void __launch_bounds__(TKW_WARPS * 32) topk_warp_kernel(const float *
 #pragma unroll 1
     for (int b = 31; b >= 0; --b) {
         const uint32_t c = T | (1u << b);
-        uint32_t n = 0;
-#pragma unroll
-        for (int i = 0; i < C; ++i) n += key[i] >= c;
-        n = __reduce_add_sync(0xFFFFFFFFu, n);
+        const uint32_t n = __reduce_add_sync(0xFFFFFFFFu, count_ge<C>(key, c));
         if (n >= kk) {
             T = c;
             if (n == kk) break;  // {key >= T} is exactly the answer
         }
     }
-    uint32_t ngt = 0;
-#pragma unroll
-    for (int i = 0; i < C; ++i) ngt += key[i] > T;
-    ngt = __reduce_add_sync(0xFFFFFFFFu, ngt);
+    // keys > T = keys >= T + 1 (T + 1 wraps to 0 only for T = 2^32 - 1, where none is greater:
+    // count_ge(0) adds 2^32 - 0 = 0 and never carries)
+    const uint32_t ngt = __reduce_add_sync(0xFFFFFFFFu, count_ge<C>(key, T + 1u));
     const uint32_t need = kk - ngt;  // keys == T to take, lowest indices first
     const uint32_t lt = (1u << lane) - 1u;
     int32_t *out = idx + (size_t)row * k;
