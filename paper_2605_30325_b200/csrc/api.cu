@@ -226,11 +226,11 @@ static veda_status tile_permute_impl(const uint16_t *x, int64_t head_stride, int
     if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "tile_permute: d=%d unsupported", d);
     if (!aligned16(x) || !aligned16(x_tiled) || (head_stride % 8) || (token_stride % 8))
         return fail(VEDA_ERR_ALIGN, "tile_permute: pointers/strides must be 16-byte aligned");
-    veda_status st = check_arch();
-    if (st != VEDA_OK) return st;
     Shape sh;
     HeadCfgs hc;
-    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // argument errors before any device call
+    if (st != VEDA_OK) return st;
+    if ((st = check_arch()) != VEDA_OK) return st;
     return launch_tile_permute(x, head_stride, token_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w,
                                sh.B, sh.NT, d, x_tiled, tile_count, slot_mask, z, S(stream));
 }
@@ -258,11 +258,11 @@ veda_status veda_tile_unpermute(const uint16_t *o_tiled, veda_latent lat, const 
     if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "tile_unpermute: d=%d unsupported", d);
     if (!aligned16(o) || !aligned16(o_tiled) || (head_stride % 8) || (token_stride % 8))
         return fail(VEDA_ERR_ALIGN, "tile_unpermute: pointers/strides must be 16-byte aligned");
-    veda_status st = check_arch();
-    if (st != VEDA_OK) return st;
     Shape sh;
     HeadCfgs hc;
-    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // argument errors before any device call
+    if (st != VEDA_OK) return st;
+    if ((st = check_arch()) != VEDA_OK) return st;
     return launch_tile_unpermute(o_tiled, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B, sh.NT, d, o,
                                  head_stride, token_stride, S(stream));
 }
@@ -409,11 +409,11 @@ veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int64_t token
     if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "tile_pool: d=%d unsupported", d);
     if (!aligned16(x) || (head_stride % 8) || (token_stride % 8))
         return fail(VEDA_ERR_ALIGN, "tile_pool: pointer/strides must be 16-byte aligned");
-    veda_status st = check_arch();
-    if (st != VEDA_OK) return st;
     Shape sh;
     HeadCfgs hc;
-    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // argument errors before any device call
+    if (st != VEDA_OK) return st;
+    if ((st = check_arch()) != VEDA_OK) return st;
     return launch_tile_pool_tokens(x, head_stride, token_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
                                    sh.NT, d, z, tile_count, slot_mask, S(stream));
 }
@@ -429,11 +429,11 @@ veda_status veda_sparse_attn_fwd_tokens(const uint16_t *q, const uint16_t *k, co
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || (head_stride % 8) || (token_stride % 8) ||
         (o_head_stride % 8) || (o_token_stride % 8))
         return fail(VEDA_ERR_ALIGN, "sparse_attn_fwd_tokens: pointers/strides must be 16-byte aligned");
-    veda_status st = check_arch();
-    if (st != VEDA_OK) return st;
     Shape sh;
     HeadCfgs hc;
-    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // argument errors before any device call
+    if (st != VEDA_OK) return st;
+    if ((st = check_arch()) != VEDA_OK) return st;
     if (k_keep < 1 || k_keep > sh.NT)
         return fail(VEDA_ERR_K_RANGE, "sparse_attn_fwd_tokens: k=%d outside [1, %d]", k_keep, sh.NT);
     const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)d);
@@ -472,11 +472,11 @@ veda_status veda_tile_permute_scalar(const float *x, int64_t head_stride, veda_l
                                      int32_t Hh, float pad, float *x_tiled, void *stream)
 {
     if (!x || !x_tiled) return fail(VEDA_ERR_NULL, "tile_permute_scalar: NULL tensor");
-    veda_status st = check_arch();
-    if (st != VEDA_OK) return st;
     Shape sh;
     HeadCfgs hc;
-    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // argument errors before any device call
+    if (st != VEDA_OK) return st;
+    if ((st = check_arch()) != VEDA_OK) return st;
     if (head_stride < (int64_t)lat.t * lat.h * lat.w)
         return fail(VEDA_ERR_SHAPE, "tile_permute_scalar: head_stride < N");
     return launch_permute_scalar(x, head_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B, sh.NT, pad,
@@ -487,11 +487,11 @@ veda_status veda_tile_unpermute_scalar(const float *x_tiled, veda_latent lat, co
                                        float *x, int64_t head_stride, void *stream)
 {
     if (!x || !x_tiled) return fail(VEDA_ERR_NULL, "tile_unpermute_scalar: NULL tensor");
-    veda_status st = check_arch();
-    if (st != VEDA_OK) return st;
     Shape sh;
     HeadCfgs hc;
-    if ((st = shape_of(lat, cfg, Hh, &sh, &hc)) != VEDA_OK) return st;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // argument errors before any device call
+    if (st != VEDA_OK) return st;
+    if ((st = check_arch()) != VEDA_OK) return st;
     if (head_stride < (int64_t)lat.t * lat.h * lat.w)
         return fail(VEDA_ERR_SHAPE, "tile_unpermute_scalar: head_stride < N");
     return launch_unpermute_scalar(x_tiled, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B, sh.NT, x,

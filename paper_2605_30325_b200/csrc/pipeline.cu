@@ -138,11 +138,10 @@ veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k
     if (!q_host || !k_host || !v_host || !o_host || !w || !workspace)
         return fail(VEDA_ERR_NULL, "sparse_attention_host: NULL pointer");
     if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "sparse_attention_host: d=%d unsupported", d);
-    veda_status st = check_arch();
-    if (st != VEDA_OK) return st;
     Shape sh;
     HeadCfgs all;
-    if ((st = shape_of(lat, cfg, Hh, &sh, &all)) != VEDA_OK) return st;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, &all);  // argument errors before any device call
+    if (st != VEDA_OK) return st;
     if (k < 1 || k > sh.NT) return fail(VEDA_ERR_K_RANGE, "sparse_attention_host: k=%d outside [1, %d]", k, sh.NT);
     const int64_t N = (int64_t)lat.t * lat.h * lat.w;
     const bool head_major = head_stride == N * d && token_stride == d;
@@ -156,6 +155,7 @@ veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k
         return fail(VEDA_ERR_WORKSPACE, "sparse_attention_host: workspace %zu < %zu", workspace_bytes,
                     kSlots * L.total);
     if (!aligned16(workspace)) return fail(VEDA_ERR_ALIGN, "sparse_attention_host: workspace not aligned");
+    if ((st = check_arch()) != VEDA_OK) return st;
     SideStreams side;
     if ((st = side_streams(&side)) != VEDA_OK) return st;
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);

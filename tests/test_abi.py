@@ -154,3 +154,25 @@ def test_token_path_and_host_entry_errors(lib):
     st = lib.veda_sparse_attention_host(None, fake, fake, 16384, 64, lat, cfg, 1, 64, 2, ctypes.byref(w), 0, fake,
                                         fake, nb.value, None)
     assert veda.VEDA_STATUS[st] == "VEDA_ERR_NULL"
+
+
+def test_empty_inputs_rejected_before_device_work(lib):
+    """Empty problems (no heads, no tiles, an empty latent axis) are argument errors
+    (VEDA_ERR_SHAPE), reported identically with or without a GPU: every entry point
+    validates shapes before its first device call."""
+    from paper_2605_30325_b200 import veda
+
+    fake = ctypes.c_void_p(16)
+    lat, cfg = veda.Latent(4, 4, 8), veda._cfg_array([(4, 4, 8)], 1)
+    shape = lambda st: veda.VEDA_STATUS[st]  # noqa: E731
+    assert shape(lib.veda_select_topk(fake, 0, 4, 2, fake, None)) == "VEDA_ERR_SHAPE"
+    assert shape(lib.veda_select_topk(fake, 1, 0, 1, fake, None)) == "VEDA_ERR_SHAPE"
+    assert shape(lib.veda_sparse_attn_fwd(fake, fake, fake, fake, fake, 0, 4, 128, 128, 2, 0.1, fake, None,
+                                          None)) == "VEDA_ERR_SHAPE"
+    assert shape(lib.veda_tile_permute(fake, 0, 128, lat, cfg, 0, 128, fake, None, None, None)) == "VEDA_ERR_SHAPE"
+    assert shape(lib.veda_tile_permute(fake, 0, 128, veda.Latent(0, 4, 8), cfg, 1, 128, fake, None, None,
+                                       None)) == "VEDA_ERR_SHAPE"
+    assert shape(lib.veda_tile_unpermute(fake, lat, cfg, 0, 128, fake, 0, 128, None)) == "VEDA_ERR_SHAPE"
+    assert shape(lib.veda_tile_pool(fake, 16384, 128, lat, cfg, 0, 128, fake, fake, fake, None)) == "VEDA_ERR_SHAPE"
+    assert shape(lib.veda_tile_pool(fake, 16384, 128, veda.Latent(4, 0, 8), cfg, 1, 128, fake, fake, fake,
+                                    None)) == "VEDA_ERR_SHAPE"
