@@ -17,12 +17,20 @@
  *     no pointer after returning.  Host arrays are read during the call only.  The
  *     caller owns every buffer (workspace sizes come from the *_workspace helpers).
  *     Exceptions, all one-time or bounded: the first scoring call on a device uploads
- *     a 20 KB constant table (Phi for the GELU) into the library's static device
+ *     a 36 KB constant table (Phi for the GELU) into the library's static device
  *     memory and synchronises `stream` once; veda_sparse_attention_host creates two
  *     side streams per device on first use and a few events per call.
  *   - Errors are returned as veda_status; nothing is printed, thrown or aborted.
- *     veda_last_error() gives a thread-local detail string for the last failure.
- *     Faults inside a kernel surface later on the stream as CUDA errors.
+ *     Arguments (NULL pointers, shapes including empty ones, k range, alignment) are
+ *     validated before the first device call, so they report the same status with or
+ *     without a GPU.  veda_last_error() gives a thread-local detail string for the
+ *     last failure.  Faults inside a kernel surface later on the stream as CUDA errors.
+ *   - Environment, read once at library load (measured alternatives, not the default
+ *     path; profiles/r01_attn_experiments.md): VEDA_ATTN=hs|ps|1q selects another
+ *     attention schedule (ps: B = d = 128 launches; 1q: tiled-layout calls only), VEDA_SCORER=dmma the FP64-tensor-core scorer instead of the
+ *     INT8 Ozaki one (VEDA_GEMM=simt its CUDA-core GEMM), VEDA_TOPK=cta the CTA-per-row
+ *     select.  Results agree within the tolerances tests/test_gpu_parity.py states
+ *     (index lists and untiling bit-exact).
  *   - Supported: B = p_t*p_h*p_w in {64, 128}; d in {64, 128}; 1 <= k <= n_tiles;
  *     Hh <= 1024 heads per call.  Device must be sm_100 (B200).
  *
