@@ -27,9 +27,9 @@
  *     last failure.  Faults inside a kernel surface later on the stream as CUDA errors.
  *   - Environment, read once at library load (measured alternatives, not the default
  *     path; profiles/r01_attn_experiments.md): VEDA_ATTN=hs|ps|1q selects another
- *     attention schedule (ps: B = d = 128 launches; 1q: tiled-layout calls only), VEDA_SCORER=dmma the FP64-tensor-core scorer instead of the
- *     INT8 Ozaki one (VEDA_GEMM=simt its CUDA-core GEMM), VEDA_TOPK=cta the CTA-per-row
- *     select.  Results agree within the tolerances tests/test_gpu_parity.py states
+ *     attention schedule (ps: B = d = 128 launches; 1q: tiled-layout calls only),
+ *     VEDA_SCORER=dmma the FP64-tensor-core scorer instead of the INT8 Ozaki one
+ *     (VEDA_GEMM=simt its CUDA-core GEMM), VEDA_TOPK=cta the CTA-per-row select.  Results agree within the tolerances tests/test_gpu_parity.py states
  *     (index lists and untiling bit-exact).
  *   - Supported: B = p_t*p_h*p_w in {64, 128}; d in {64, 128}; 1 <= k <= n_tiles;
  *     Hh <= 1024 heads per call.  Device must be sm_100 (B200).
