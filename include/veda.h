@@ -193,6 +193,21 @@ VEDA_API veda_status veda_sparse_attn_fwd_tokens(const uint16_t *q, const uint16
                                                  float softmax_scale, uint16_t *o, int64_t o_head_stride,
                                                  int64_t o_token_stride, float *lse, void *stream);
 
+/* The same for the units [unit_begin, unit_end) of the flattened (head, query tile) space
+ * (unit u = h * n_tiles + i; SURVEY.md §8(e)'s finer multi-GPU share, for head counts that
+ * do not divide the GPU count).  All tensors are the full call's; only the output rows
+ * (and lse rows) of tokens in the range's query tiles are written, each exactly as the
+ * full call writes them, so the shares of a partition of [0, Hh*n_tiles) together produce
+ * the full call's output bit for bit.  0 <= unit_begin <= unit_end <= Hh*n_tiles, else
+ * VEDA_ERR_SHAPE; an empty range enqueues nothing. */
+VEDA_API veda_status veda_sparse_attn_fwd_tokens_units(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                                                       int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                                       const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh,
+                                                       int32_t d, const int32_t *idx, const uint32_t *slot_mask,
+                                                       int32_t k_keep, float softmax_scale, uint16_t *o,
+                                                       int64_t o_head_stride, int64_t o_token_stride, float *lse,
+                                                       int32_t unit_begin, int32_t unit_end, void *stream);
+
 /* ---- the whole path on HOST buffers (end-to-end call) ------------------------------ */
 
 /* Device workspace veda_sparse_attention_host needs (two buffer sets of one head chunk:

@@ -418,11 +418,12 @@ veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int64_t token
                                    sh.NT, d, z, tile_count, slot_mask, S(stream));
 }
 
-veda_status veda_sparse_attn_fwd_tokens(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t head_stride,
-                                        int64_t token_stride, veda_latent lat, const veda_tile_cfg *cfg, int32_t Hh,
-                                        int32_t d, const int32_t *idx, const uint32_t *slot_mask, int32_t k_keep,
-                                        float softmax_scale, uint16_t *o, int64_t o_head_stride,
-                                        int64_t o_token_stride, float *lse, void *stream)
+static veda_status sparse_attn_fwd_tokens_impl(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                                               int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                               const veda_tile_cfg *cfg, int32_t Hh, int32_t d, const int32_t *idx,
+                                               const uint32_t *slot_mask, int32_t k_keep, float softmax_scale,
+                                               uint16_t *o, int64_t o_head_stride, int64_t o_token_stride, float *lse,
+                                               bool all_units, int32_t unit_begin, int32_t unit_end, void *stream)
 {
     if (!q || !k || !v || !idx || !slot_mask || !o) return fail(VEDA_ERR_NULL, "sparse_attn_fwd_tokens: NULL pointer");
     if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "sparse_attn_fwd_tokens: d=%d unsupported", d);
@@ -433,13 +434,44 @@ veda_status veda_sparse_attn_fwd_tokens(const uint16_t *q, const uint16_t *k, co
     HeadCfgs hc;
     veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // argument errors before any device call
     if (st != VEDA_OK) return st;
-    if ((st = check_arch()) != VEDA_OK) return st;
     if (k_keep < 1 || k_keep > sh.NT)
         return fail(VEDA_ERR_K_RANGE, "sparse_attn_fwd_tokens: k=%d outside [1, %d]", k_keep, sh.NT);
+    const int32_t n_units = Hh * sh.NT;
+    if (all_units) {
+        unit_begin = 0;
+        unit_end = n_units;
+    } else if (unit_begin < 0 || unit_begin > unit_end || unit_end > n_units) {
+        return fail(VEDA_ERR_SHAPE, "sparse_attn_fwd_tokens_units: [%d, %d) outside [0, %d]", unit_begin, unit_end,
+                    n_units);
+    }
+    if ((st = check_arch()) != VEDA_OK) return st;
+    if (unit_begin == unit_end) return VEDA_OK;  // an empty share (e.g. a rank without units)
     const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)d);
     return launch_sparse_attn_tok(q, k, v, head_stride, token_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w,
                                   sh.B, sh.NT, d, idx, slot_mask, k_keep, scale, o, o_head_stride, o_token_stride, lse,
-                                  S(stream));
+                                  unit_begin, unit_end, S(stream));
+}
+
+veda_status veda_sparse_attn_fwd_tokens(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t head_stride,
+                                        int64_t token_stride, veda_latent lat, const veda_tile_cfg *cfg, int32_t Hh,
+                                        int32_t d, const int32_t *idx, const uint32_t *slot_mask, int32_t k_keep,
+                                        float softmax_scale, uint16_t *o, int64_t o_head_stride,
+                                        int64_t o_token_stride, float *lse, void *stream)
+{
+    return sparse_attn_fwd_tokens_impl(q, k, v, head_stride, token_stride, lat, cfg, Hh, d, idx, slot_mask, k_keep,
+                                       softmax_scale, o, o_head_stride, o_token_stride, lse, true, 0, 0, stream);
+}
+
+veda_status veda_sparse_attn_fwd_tokens_units(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                                              int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                              const veda_tile_cfg *cfg, int32_t Hh, int32_t d, const int32_t *idx,
+                                              const uint32_t *slot_mask, int32_t k_keep, float softmax_scale,
+                                              uint16_t *o, int64_t o_head_stride, int64_t o_token_stride, float *lse,
+                                              int32_t unit_begin, int32_t unit_end, void *stream)
+{
+    return sparse_attn_fwd_tokens_impl(q, k, v, head_stride, token_stride, lat, cfg, Hh, d, idx, slot_mask, k_keep,
+                                       softmax_scale, o, o_head_stride, o_token_stride, lse, false, unit_begin,
+                                       unit_end, stream);
 }
 
 veda_status veda_target_scores(const uint16_t *q_tiled, const uint16_t *k_tiled, const uint32_t *slot_mask,

@@ -27,7 +27,8 @@ struct Params {
     const uint32_t *slot_mask;
     uint16_t *out;
     float *lse;
-    int NT, k, total_units;
+    int NT, k, total_units;  // units (head, query tile) of this launch: [unit0, unit0 + total_units)
+    int unit0;
     float scale_log2;
     unsigned long long *trace;  // VEDA_ATTN_TRACE builds only: per-step clock64 stamps of CTA 0
 };

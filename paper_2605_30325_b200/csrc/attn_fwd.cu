@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -110,11 +111,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
 
-    const int NT = p.NT, K = p.k, total = p.total_units;
+    const int NT = p.NT, K = p.k, total = p.unit0 + p.total_units;  // units end
     const int gslots = gridDim.x * NSLOT;
-    const int rounds = (total + gslots - 1) / gslots;
+    const int rounds = (p.total_units + gslots - 1) / gslots;
     // unit u = h*NT + i; consecutive CTAs/slots take consecutive query tiles of one head (L2 reuse)
-#define UNIT_OF(r, s) ((r) * gslots + blockIdx.x * NSLOT + (s))
+#define UNIT_OF(r, s) (p.unit0 + (r) * gslots + blockIdx.x * NSLOT + (s))
 
     if (warp < 4) {
 #ifndef VEDA_NO_SETMAXNREG
@@ -514,6 +515,7 @@ static Params make_params(const int32_t *idx, const uint32_t *mask, uint16_t *o,
     p.NT = NT;
     p.k = kk;
     p.total_units = Hh * NT;
+    p.unit0 = 0;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.trace = g_attn_trace;
     return p;
@@ -541,7 +543,7 @@ template <int B, int D>
 static veda_status launch_tok(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t hs, int64_t ts,
                               const HeadCfgs &cf, int Hh, int Hp, int Wp, int T, int H, int W, int NT,
                               const int32_t *idx, const uint32_t *mask, int kk, float scale, uint16_t *o,
-                              int64_t o_hs, int64_t o_ts, float *lse, cudaStream_t stream)
+                              int64_t o_hs, int64_t o_ts, float *lse, int u_begin, int u_end, cudaStream_t stream)
 {
     static TokParams tp;  // host staging (3-4 KB): filled per launch, passed by value
     CUtensorMap dummy;
@@ -560,6 +562,12 @@ static veda_status launch_tok(const uint16_t *q, const uint16_t *k, const uint16
             tp.cid[h1 - h0] = (uint8_t)c;
         }
         const int hn = h1 - h0;
+        // units of this head group that fall in [u_begin, u_end) (flattened head x query tile)
+        const int g_lo = std::max(u_begin, h0 * NT), g_hi = std::min(u_end, h1 * NT);
+        if (g_lo >= g_hi) {
+            h0 = h1;
+            continue;
+        }
         veda_status st;
         int tm = 0;
         for (int c = 0; c < nc; ++c) {
@@ -585,9 +593,11 @@ static veda_status launch_tok(const uint16_t *q, const uint16_t *k, const uint16
         tp.tok_major = tm;
         tp.o_hs = o_hs;
         tp.o_ts = o_ts;
-        const Params p = make_params(idx + (size_t)h0 * NT * kk, mask + (size_t)h0 * NT * MW, o + (size_t)h0 * o_hs,
-                                     lse ? lse + (size_t)h0 * NT * B : nullptr, hn, NT, kk, scale);
-        if ((st = launch_kernel<B, D, true>(dummy, dummy, dummy, p, tp, hn * NT, stream)) != VEDA_OK) return st;
+        Params p = make_params(idx + (size_t)h0 * NT * kk, mask + (size_t)h0 * NT * MW, o + (size_t)h0 * o_hs,
+                               lse ? lse + (size_t)h0 * NT * B : nullptr, hn, NT, kk, scale);
+        p.unit0 = g_lo - h0 * NT;
+        p.total_units = g_hi - g_lo;
+        if ((st = launch_kernel<B, D, true>(dummy, dummy, dummy, p, tp, p.total_units, stream)) != VEDA_OK) return st;
         h0 = h1;
     }
     return VEDA_OK;
@@ -621,7 +631,8 @@ veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint1
 veda_status launch_sparse_attn_tok(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t hs, int64_t ts,
                                    const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp, int T, int H, int W, int B,
                                    int NT, int d, const int32_t *idx, const uint32_t *mask, int kk, float scale,
-                                   uint16_t *o, int64_t o_hs, int64_t o_ts, float *lse, cudaStream_t s)
+                                   uint16_t *o, int64_t o_hs, int64_t o_ts, float *lse, int u_begin, int u_end,
+                                   cudaStream_t s)
 {
     (void)Tp;
     // a stride that is never used (one token, or one head) may equal the other one; give it
@@ -634,7 +645,7 @@ veda_status launch_sparse_attn_tok(const uint16_t *q, const uint16_t *k, const u
         else
             return fail(VEDA_ERR_ALIGN, "sparse_attn_fwd_tokens: head_stride == token_stride");
     }
-#define VEDA_TOK_ARGS q, k, v, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, idx, mask, kk, scale, o, o_hs, o_ts, lse, s
+#define VEDA_TOK_ARGS q, k, v, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, idx, mask, kk, scale, o, o_hs, o_ts, lse, u_begin, u_end, s
     if (B == 128 && d == 128) return attn::launch_tok<128, 128>(VEDA_TOK_ARGS);
     if (B == 128 && d == 64) return attn::launch_tok<128, 64>(VEDA_TOK_ARGS);
     if (B == 64 && d == 128) return attn::launch_tok<64, 128>(VEDA_TOK_ARGS);

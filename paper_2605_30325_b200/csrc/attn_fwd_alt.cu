@@ -106,10 +106,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
-    const int NT = p.NT, K = p.k, total = p.total_units;
+    const int NT = p.NT, K = p.k, total = p.unit0 + p.total_units;  // units end
     const int gslots = gridDim.x * NSLOT;
-    const int rounds = (total + gslots - 1) / gslots;
-#define H_UNIT(r, s) ((r) * gslots + blockIdx.x * NSLOT + (s))
+    const int rounds = (p.total_units + gslots - 1) / gslots;
+#define H_UNIT(r, s) (p.unit0 + (r) * gslots + blockIdx.x * NSLOT + (s))
 
     if (warp < 4) {
 #ifndef VEDA_NO_SETMAXNREG
@@ -544,10 +544,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
-    const int NT = p.NT, K = p.k, total = p.total_units;
+    const int NT = p.NT, K = p.k, total = p.unit0 + p.total_units;  // units end
     const int gslots = gridDim.x * NSLOT;
-    const int rounds = (total + gslots - 1) / gslots;
-#define X_UNIT(r, s) ((r) * gslots + blockIdx.x * NSLOT + (s))
+    const int rounds = (p.total_units + gslots - 1) / gslots;
+#define X_UNIT(r, s) (p.unit0 + (r) * gslots + blockIdx.x * NSLOT + (s))
 
     if (warp < 4) {
 #ifndef VEDA_NO_SETMAXNREG

@@ -69,7 +69,8 @@ veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint1
 veda_status launch_sparse_attn_tok(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t hs, int64_t ts,
                                    const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp, int T, int H, int W, int B,
                                    int NT, int d, const int32_t *idx, const uint32_t *mask, int kk, float scale,
-                                   uint16_t *o, int64_t o_hs, int64_t o_ts, float *lse, cudaStream_t s);
+                                   uint16_t *o, int64_t o_hs, int64_t o_ts, float *lse, int u_begin, int u_end,
+                                   cudaStream_t s);  // units [u_begin, u_end) of the flattened (head, query tile) space
 veda_status launch_tile_pool_tokens(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfgs &cf, int Hh, int Tp,
                                     int Hp, int Wp, int T, int H, int W, int B, int NT, int d, float *z,
                                     int32_t *cnt, uint32_t *mask, cudaStream_t s);

@@ -226,7 +226,8 @@ veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k
         if (c >= kSlots) VEDA_CU(cudaStreamWaitEvent(cs, ev_d2h[c - kSlots], 0));  // out slot drained
         const float scale = 1.0f / std::sqrt((float)d);
         if ((st = launch_sparse_attn_tok(in[0], in[1], in[2], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h,
-                                         lat.w, sh.B, sh.NT, d, idx, mask, k, scale, out, dhs, dts, nullptr, cs)) !=
+                                         lat.w, sh.B, sh.NT, d, idx, mask, k, scale, out, dhs, dts, nullptr, 0,
+                                         hn * sh.NT, cs)) !=
             VEDA_OK)
             return st;
         VEDA_CU(cudaEventRecord(ev_infree[c], cs));  // the attention was the last reader of Q/K/V

@@ -30,7 +30,7 @@ EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_worksp
            "veda_launch_count", "veda_check_device", "veda_tile_permute_pool", "veda_tile_score_pooled",
            "veda_target_scores", "veda_tile_recall", "veda_tile_permute_scalar", "veda_tile_unpermute_scalar",
            "veda_sq_err", "veda_sparse_attention_host_workspace", "veda_sparse_attention_host",
-           "veda_tile_pool", "veda_sparse_attn_fwd_tokens"]
+           "veda_tile_pool", "veda_sparse_attn_fwd_tokens", "veda_sparse_attn_fwd_tokens_units"]
 
 
 class VedaError(RuntimeError):
@@ -92,6 +92,8 @@ def load(path: str = LIB_PATH):
         "veda_tile_pool": ([P, i64, i64, Latent, P, i32, i32, P, P, P, P], i32),
         "veda_sparse_attn_fwd_tokens": ([P, P, P, i64, i64, Latent, P, i32, i32, P, P, i32, f32, P, i64, i64, P, P],
                                         i32),
+        "veda_sparse_attn_fwd_tokens_units": ([P, P, P, i64, i64, Latent, P, i32, i32, P, P, i32, f32, P, i64, i64, P,
+                                               i32, i32, P], i32),
         "veda_status_str": ([i32], ctypes.c_char_p),
         "veda_last_error": ([], ctypes.c_char_p),
         "veda_launch_count": ([], ctypes.c_uint64),
@@ -372,9 +374,12 @@ def tile_pool(x: torch.Tensor, lat, cfgs, z=None, meta=True):
     return z, cnt, mask
 
 
-def sparse_attn_fwd_tokens(q, k, v, lat, cfgs, idx, slot_mask, scale: float = 0.0, out=None, want_lse=False):
+def sparse_attn_fwd_tokens(q, k, v, lat, cfgs, idx, slot_mask, scale: float = 0.0, out=None, want_lse=False,
+                           units=None):
     """Attention + untiling straight on token tensors [Hh, N, d] (veda_sparse_attn_fwd_tokens).
-    Rows of padded slots are not written, so ``out`` (default: zeros) keeps its values there."""
+    Rows of padded slots are not written, so ``out`` (default: zeros) keeps its values there.
+    ``units=(begin, end)`` computes only that range of the flattened (head, query tile) space
+    (veda_sparse_attn_fwd_tokens_units); rows outside it are not written either."""
     _need_cuda(q, k, v, idx, slot_mask)
     Hh, N, d = q.shape
     if not (k.stride() == q.stride() and v.stride() == q.stride()):
@@ -384,10 +389,12 @@ def sparse_attn_fwd_tokens(q, k, v, lat, cfgs, idx, slot_mask, scale: float = 0.
     if out is None:
         out = torch.zeros((Hh, N, d), dtype=torch.bfloat16, device=q.device)
     lse = torch.empty((Hh, NT, B), dtype=torch.float32, device=q.device) if want_lse else None
-    st = load().veda_sparse_attn_fwd_tokens(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), Latent(*lat),
-                                            _cfg_array(cfgs, Hh), Hh, d, _ptr(idx), _ptr(slot_mask), kk,
-                                            float(scale), _ptr(out), out.stride(0), out.stride(1), _ptr(lse),
-                                            _stream())
+    args = (_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), Latent(*lat), _cfg_array(cfgs, Hh), Hh, d,
+            _ptr(idx), _ptr(slot_mask), kk, float(scale), _ptr(out), out.stride(0), out.stride(1), _ptr(lse))
+    if units is None:
+        st = load().veda_sparse_attn_fwd_tokens(*args, _stream())
+    else:
+        st = load().veda_sparse_attn_fwd_tokens_units(*args, int(units[0]), int(units[1]), _stream())
     _check(st, "sparse_attn_fwd_tokens")
     return (out, lse) if want_lse else out
 

@@ -87,6 +87,68 @@ def test_head_range_partition():
     assert [len(shard.head_range(24, r, 8)) for r in range(8)] == [3] * 8
 
 
+def test_unit_range_partition():
+    """The finer (head x query tile) share: every unit exactly once, sizes within one, and
+    the heads a share touches are exactly those of its units."""
+    from paper_2605_30325_b200 import shard
+
+    for Hh, NT in ((12, 336), (24, 1920), (3, 7), (1, 5), (40, 720)):
+        for G in (1, 2, 3, 4, 8):
+            parts = [shard.unit_range(Hh, NT, r, G) for r in range(G)]
+            assert sum((list(p) for p in parts), []) == list(range(Hh * NT))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= 1
+            for p in parts:
+                assert list(shard.heads_of_units(p, NT)) == sorted({u // NT for u in p})
+    # Wan-1.3B on 8 GPUs: head sharding leaves the busiest rank 2 of 12 heads, units 1.5
+    assert max(len(shard.head_range(12, r, 8)) for r in range(8)) == 2
+    assert max(len(shard.unit_range(12, 336, r, 8)) for r in range(8)) == 12 * 336 // 8
+
+
+def _unit_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_30325_b200 import shard
+
+    import oracle
+
+    oracle.build()
+    full = _path_for_heads(list(range(len(CFGS))))  # every rank may read the inputs of any head
+    NT = full["o"].shape[1]
+    units = shard.unit_range(len(CFGS), NT, rank, world)
+    heads = shard.heads_of_units(units, NT)
+    res = _path_for_heads(list(heads))  # scores / lists / attention of the touched heads only
+    share = {}
+    for u in units:
+        h, i = divmod(u, NT)
+        share[u] = (res["idx"][h - heads.start][i], res["o"][h - heads.start][i])
+    gathered = [None] * world
+    dist.all_gather_object(gathered, share)
+    if rank == 0:
+        merged = {}
+        for g in gathered:
+            assert not (set(g) & set(merged))  # disjoint shares
+            merged.update(g)
+        np.save(os.path.join(out_dir, "units.npy"), np.array(sorted(merged)))
+        np.save(os.path.join(out_dir, "idx.npy"), np.stack([merged[u][0] for u in sorted(merged)]))
+        np.save(os.path.join(out_dir, "o.npy"), np.stack([merged[u][1] for u in sorted(merged)]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_unit_shares_equal_single(tmp_path):
+    """Unit (head x query tile) shares, assembled, equal the single-process call unit by unit
+    (world size 2: the split falls inside a head, whose K side both ranks then compute)."""
+    world, port = 2, _free_port()
+    mp.spawn(_unit_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    single = _path_for_heads(list(range(len(CFGS))))
+    Hh, NT = single["o"].shape[:2]
+    assert np.array_equal(np.load(tmp_path / "units.npy"), np.arange(Hh * NT))
+    assert np.array_equal(np.load(tmp_path / "idx.npy"), single["idx"].reshape(Hh * NT, -1))
+    assert np.array_equal(np.load(tmp_path / "o.npy"), single["o"].reshape((Hh * NT,) + single["o"].shape[2:]),
+                          equal_nan=True)
+
+
 def test_gloo_world2_sharded_equals_single(tmp_path):
     world, port = 2, _free_port()
     mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)

@@ -370,6 +370,46 @@ def test_attention_tokens_equals_tiled(V, name):
         assert torch.equal(lse, lse2)
 
 
+@pytest.mark.parametrize("name", ["toy_b128", "mixed_cfgs", "b128_d64", "wan_slice", "many_cfgs"])
+def test_attention_unit_shares_equal_full_call(V, name):
+    """veda_sparse_attn_fwd_tokens_units over a partition of the (head, query tile) units
+    (rank shares at G = 2, 3, 8, splits inside heads and head groups) writes, together,
+    exactly the full call's output and lse, bit for bit; an empty share writes nothing and
+    out-of-range shares are VEDA_ERR_SHAPE."""
+    from paper_2605_30325_b200 import shard, synth
+
+    if name == "many_cfgs":
+        c = Case("mixed_cfgs", lat=(9, 10, 13), cfgs=_many_cfg_case(64, 12), d=64, Hh=12, k=7)
+    else:
+        c = Case(name, **CASES[name])
+    dev = torch.device("cuda")
+    q, k, v = (t.to(dev) for t in (c.q, c.k, c.v))
+    _, _, mask = V.tile_permute(q, c.lat, c.cfgs)
+    NT = mask.shape[1]
+    kk = c.k_keep if c.k_keep is not None else V.k_for_sparsity(NT, c.sparsity)
+    idx = synth.random_index_lists(c.Hh, NT, kk, seed_parts=("units", name)).to(dev)
+    want, lse_w = V.sparse_attn_fwd_tokens(q, k, v, c.lat, c.cfgs, idx, mask, out=torch.full_like(q, 7.0),
+                                           want_lse=True)
+    for G in (2, 3, 8):
+        out = torch.full_like(q, 7.0)
+        lse = None
+        for r in range(G):
+            u = shard.unit_range(c.Hh, NT, r, G)
+            got, l_r = V.sparse_attn_fwd_tokens(q, k, v, c.lat, c.cfgs, idx, mask, out=out, want_lse=True,
+                                                units=(u.start, u.stop))
+            lse = l_r if lse is None else lse
+            lse.view(-1, lse.shape[-1])[u.start:u.stop] = l_r.view(-1, l_r.shape[-1])[u.start:u.stop]
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), want.view(torch.int16)), G
+        assert torch.equal(lse, lse_w), G
+    before = out.clone()
+    V.sparse_attn_fwd_tokens(q, k, v, c.lat, c.cfgs, idx, mask, out=out, units=(5, 5))
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), before.view(torch.int16))
+    with pytest.raises(V.VedaError, match="SHAPE"):
+        V.sparse_attn_fwd_tokens(q, k, v, c.lat, c.cfgs, idx, mask, out=out, units=(0, c.Hh * NT + 1))
+
+
 @pytest.mark.parametrize("preset,head_aware", [("waver12b", False), ("wan14b", False), ("wan1.3b", False),
                                                 ("waver12b", True)])
 def test_full_size_sampled(V, oracle, preset, head_aware):
