@@ -454,9 +454,15 @@ class SparseAttention:
              "tiled": ("permute", "score", "topk", "attn", "unpermute")}
 
     def __init__(self, lat, cfgs, Hh, d, scorer_weights: dict, sparsity=None, k=None, device="cuda",
-                 mode="tokens"):
+                 mode="tokens", units=None):
+        """``units=(begin, end)`` (tokens mode): the attention step computes only that range of
+        the flattened (head, query tile) units of these Hh heads (a rank's share under
+        shard.unit_range); pooling, scoring and top-k still cover the Hh heads."""
         if mode not in self.STEPS:
             raise VedaError(f"mode must be one of {list(self.STEPS)}")
+        if units is not None and mode != "tokens":
+            raise VedaError("units: tokens mode only")
+        self.units = None if units is None else (int(units[0]), int(units[1]))
         self.lat, self.cfgs, self.Hh, self.d, self.mode = tuple(lat), list(cfgs), Hh, d, mode
         self.shape = tiled_shape(lat, cfgs, Hh)
         NT, B = self.shape.n_tiles, self.shape.B
@@ -513,9 +519,16 @@ class SparseAttention:
             mark(2)
             _check(lib.veda_select_topk(_ptr(self.scores), Hh, NT, self.k, _ptr(self.idx), s), "select_topk")
             mark(3)
-            _check(lib.veda_sparse_attn_fwd_tokens(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat, cfg,
-                                                   Hh, d, _ptr(self.idx), _ptr(self.mask), self.k, 0.0, _ptr(out),
-                                                   out.stride(0), out.stride(1), None, s), "sparse_attn_fwd_tokens")
+            if self.units is None:
+                _check(lib.veda_sparse_attn_fwd_tokens(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat, cfg,
+                                                       Hh, d, _ptr(self.idx), _ptr(self.mask), self.k, 0.0, _ptr(out),
+                                                       out.stride(0), out.stride(1), None, s), "sparse_attn_fwd_tokens")
+            else:
+                _check(lib.veda_sparse_attn_fwd_tokens_units(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat,
+                                                             cfg, Hh, d, _ptr(self.idx), _ptr(self.mask), self.k, 0.0,
+                                                             _ptr(out), out.stride(0), out.stride(1), None,
+                                                             self.units[0], self.units[1], s),
+                       "sparse_attn_fwd_tokens_units")
             mark(4)
             mark(5)
             return out

@@ -5,7 +5,9 @@ For each workload (latent shape, heads) and sparsity: ms per call of the whole p
 executed TFLOP/s, and the same attention kernel run dense (k = N_T, i.e. 0 % sparsity;
 timed once per workload) -> speedup vs dense.  With --shards, also the call time of the
 busiest rank of a G-way head-sharded run (ceil(Hh/G) heads; the path has no collective,
-so this is the rank-local work) -- measured on ONE B200, not a multi-GPU measurement.
+so this is the rank-local work) -- measured on ONE B200, not a multi-GPU measurement;
+where G does not divide the head count, also the busiest rank of the (head x query tile)
+unit shares (shard.unit_range, veda_sparse_attn_fwd_tokens_units).
 Writes JSON + markdown.
 
     python tools/sweep.py [--out profiles/r01_sweep] [--workloads wan1.3b,wan14b,waver12b,...]
@@ -18,7 +20,7 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2605_30325_b200 import synth, veda  # noqa: E402
+from paper_2605_30325_b200 import shard, synth, veda  # noqa: E402
 
 # SURVEY.md §8(d) d2 shapes (24 heads, d = 128, tile (4,4,8)) plus the three model presets
 SHAPES = {
@@ -86,6 +88,19 @@ def main():
                     pr = veda.SparseAttention(lat, [pre.cfg], hr, 128, wr, sparsity=sp, device=dev)
                     r[f"rank_ms_G{G}"] = round(timeit(lambda: pr(q[:hr], k[:hr], v[:hr], out=out[:hr]), a.reps), 3)
                     del pr
+                    if heads % G:  # unit shares (shard.unit_range): the busiest rank over all G
+                        worst = 0.0
+                        for rk in range(G):
+                            u = shard.unit_range(heads, NT, rk, G)
+                            hs = shard.heads_of_units(u, NT)
+                            wr = {n: t[hs.start:hs.stop] for n, t in w.items()}
+                            loc = (u.start - hs.start * NT, u.stop - hs.start * NT)
+                            pr = veda.SparseAttention(lat, [pre.cfg], len(hs), 128, wr, sparsity=sp, device=dev,
+                                                      units=loc)
+                            sl = slice(hs.start, hs.stop)
+                            worst = max(worst, timeit(lambda: pr(q[sl], k[sl], v[sl], out=out[sl]), a.reps))
+                            del pr
+                        r[f"rank_ms_G{G}_units"] = round(worst, 3)
             rows.append(r)
             print(json.dumps(r), flush=True)
         del q, k, v, w, out
@@ -101,7 +116,9 @@ def main():
             f.write(f"| {r['workload']} | {r['tokens']} | {r['heads']} | {r['n_tiles']} | {r['sparsity']:.2f} | "
                     f"{r['k']} | {r['call_ms']} | {r['attn_ms']} | {r['attn_tflops']} | {r['dense_attn_ms']} | "
                     f"{r['dense_tflops']} | {r['speedup_call_vs_dense_kernel']} |" +
-                    "".join(f" {r[f'rank_ms_G{G}']} |" for G in gs) + "\n")
+                    "".join(f" {r[f'rank_ms_G{G}']}" + (f" (units: {r[f'rank_ms_G{G}_units']})"
+                                                        if f"rank_ms_G{G}_units" in r else "") + " |" for G in gs) +
+                    "\n")
 
 
 if __name__ == "__main__":
