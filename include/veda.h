@@ -174,6 +174,17 @@ VEDA_API veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int6
                                     veda_latent lat, const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh,
                                     int32_t d, float *z, int32_t *tile_count, uint32_t *slot_mask, void *stream);
 
+/* veda_tile_pool for the heads [head_begin, head_end) of an Hh-head call: the padded grid
+ * (hence n_tiles and every tile) is the whole call's -- the lcm of ALL Hh heads' tile
+ * extents -- and z / tile_count / slot_mask are the whole call's arrays, of which only the
+ * rows of heads in the range are written, bit-identical to veda_tile_pool's.  A rank of a
+ * (head x query tile) unit share pools the heads its units touch with it.
+ * 0 <= head_begin <= head_end <= Hh, else VEDA_ERR_SHAPE; an empty range enqueues nothing. */
+VEDA_API veda_status veda_tile_pool_heads(const uint16_t *x, int64_t head_stride, int64_t token_stride,
+                                          veda_latent lat, const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh,
+                                          int32_t d, int32_t head_begin, int32_t head_end, float *z,
+                                          int32_t *tile_count, uint32_t *slot_mask, void *stream);
+
 /* Step 4 + step 5 on the token layout: Eq. 2 for every (head, query
  * tile), the query tile and the kept key / value tiles fetched straight from q, k, v in
  * token order by one TMA box per tile (padded slots zero-filled, reading R4), and each

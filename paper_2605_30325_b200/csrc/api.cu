@@ -418,6 +418,36 @@ veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int64_t token
                                    sh.NT, d, z, tile_count, slot_mask, S(stream));
 }
 
+veda_status veda_tile_pool_heads(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                 const veda_tile_cfg *cfg, int32_t Hh, int32_t d, int32_t head_begin,
+                                 int32_t head_end, float *z, int32_t *tile_count, uint32_t *slot_mask, void *stream)
+{
+    if (!x || !z) return fail(VEDA_ERR_NULL, "tile_pool_heads: NULL pointer");
+    if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "tile_pool_heads: d=%d unsupported", d);
+    if (!aligned16(x) || (head_stride % 8) || (token_stride % 8))
+        return fail(VEDA_ERR_ALIGN, "tile_pool_heads: pointer/strides must be 16-byte aligned");
+    Shape sh;
+    HeadCfgs hc;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // the whole call's padded grid
+    if (st != VEDA_OK) return st;
+    if (head_begin < 0 || head_begin > head_end || head_end > Hh)
+        return fail(VEDA_ERR_SHAPE, "tile_pool_heads: [%d, %d) outside [0, %d]", head_begin, head_end, Hh);
+    if ((st = check_arch()) != VEDA_OK) return st;
+    if (head_begin == head_end) return VEDA_OK;
+    HeadCfgs sub;
+    const int hn = head_end - head_begin;
+    for (int h = 0; h < hn; ++h) {
+        sub.pt[h] = hc.pt[head_begin + h];
+        sub.ph[h] = hc.ph[head_begin + h];
+        sub.pw[h] = hc.pw[head_begin + h];
+    }
+    const size_t h0 = (size_t)head_begin;
+    return launch_tile_pool_tokens(x + h0 * head_stride, head_stride, token_stride, sub, hn, sh.Tp, sh.Hp, sh.Wp, lat.t,
+                                   lat.h, lat.w, sh.B, sh.NT, d, z + h0 * sh.NT * 3 * d,
+                                   tile_count ? tile_count + h0 * sh.NT : nullptr,
+                                   slot_mask ? slot_mask + h0 * sh.NT * (sh.B / 32) : nullptr, S(stream));
+}
+
 static veda_status sparse_attn_fwd_tokens_impl(const uint16_t *q, const uint16_t *k, const uint16_t *v,
                                                int64_t head_stride, int64_t token_stride, veda_latent lat,
                                                const veda_tile_cfg *cfg, int32_t Hh, int32_t d, const int32_t *idx,

@@ -30,7 +30,8 @@ EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_worksp
            "veda_launch_count", "veda_check_device", "veda_tile_permute_pool", "veda_tile_score_pooled",
            "veda_target_scores", "veda_tile_recall", "veda_tile_permute_scalar", "veda_tile_unpermute_scalar",
            "veda_sq_err", "veda_sparse_attention_host_workspace", "veda_sparse_attention_host",
-           "veda_tile_pool", "veda_sparse_attn_fwd_tokens", "veda_sparse_attn_fwd_tokens_units"]
+           "veda_tile_pool", "veda_sparse_attn_fwd_tokens", "veda_sparse_attn_fwd_tokens_units",
+           "veda_tile_pool_heads"]
 
 
 class VedaError(RuntimeError):
@@ -90,6 +91,7 @@ def load(path: str = LIB_PATH):
         "veda_sparse_attention_host_workspace": ([Latent, P, i32, i32, i32, P, i32, P], i32),
         "veda_sparse_attention_host": ([P, P, P, i64, i64, Latent, P, i32, i32, i32, P, i32, P, P, sz, P], i32),
         "veda_tile_pool": ([P, i64, i64, Latent, P, i32, i32, P, P, P, P], i32),
+        "veda_tile_pool_heads": ([P, i64, i64, Latent, P, i32, i32, i32, i32, P, P, P, P], i32),
         "veda_sparse_attn_fwd_tokens": ([P, P, P, i64, i64, Latent, P, i32, i32, P, P, i32, f32, P, i64, i64, P, P],
                                         i32),
         "veda_sparse_attn_fwd_tokens_units": ([P, P, P, i64, i64, Latent, P, i32, i32, P, P, i32, f32, P, i64, i64, P,
@@ -455,9 +457,12 @@ class SparseAttention:
 
     def __init__(self, lat, cfgs, Hh, d, scorer_weights: dict, sparsity=None, k=None, device="cuda",
                  mode="tokens", units=None):
-        """``units=(begin, end)`` (tokens mode): the attention step computes only that range of
-        the flattened (head, query tile) units of these Hh heads (a rank's share under
-        shard.unit_range); pooling, scoring and top-k still cover the Hh heads."""
+        """``units=(begin, end)`` (tokens mode): a rank's share under shard.unit_range of the
+        flattened (head, query tile) units of this Hh-head call.  Pooling (on the call's
+        padded grid, veda_tile_pool_heads), scoring and top-k then run for the heads the
+        share touches only, and the attention for the share's units only
+        (veda_sparse_attn_fwd_tokens_units); q, k, v, out stay the whole call's tensors and
+        only the share's output rows are written."""
         if mode not in self.STEPS:
             raise VedaError(f"mode must be one of {list(self.STEPS)}")
         if units is not None and mode != "tokens":
@@ -481,7 +486,18 @@ class SparseAttention:
         self.mask = torch.empty((Hh, NT, B // 32), dtype=torch.int32, device=dev)
         self.scores = torch.empty((Hh, NT, NT), dtype=torch.float32, device=dev)
         self.idx = torch.empty((Hh, NT, self.k), dtype=torch.int32, device=dev)
-        self.ws = ScoreWorkspace(Hh, NT, d, self.scorer, dev)
+        self.heads = range(Hh)
+        if self.units is not None:
+            from .shard import heads_of_units
+
+            if not (0 <= self.units[0] <= self.units[1] <= Hh * NT):
+                raise VedaError(f"units {self.units} outside [0, {Hh * NT}]")
+            self.heads = heads_of_units(range(*self.units), NT)
+            h0, h1 = self.heads.start, self.heads.stop
+            self.w_sub = {n: t[h0:h1] for n, t in scorer_weights.items()}
+            if h1 > h0:
+                self.scorer = make_scorer(self.w_sub)
+        self.ws = ScoreWorkspace(max(1, len(self.heads)), NT, d, self.scorer, dev)
 
     def tiled(self, q, k, v):
         """Tiled copies (q~, k~, v~) of the inputs (for the oracle-mask / target tools)."""
@@ -508,16 +524,26 @@ class SparseAttention:
         if self.mode == "tokens":
             if not (k.stride() == q.stride() and v.stride() == q.stride()):
                 raise VedaError("q, k, v must share strides")
-            _check(lib.veda_tile_pool(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, _ptr(self.zq),
-                                      _ptr(self.cnt), _ptr(self.mask), s), "tile_pool(q)")
-            _check(lib.veda_tile_pool(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, _ptr(self.zk), None, None,
-                                      s), "tile_pool(k)")
+            h0, h1 = self.heads.start, self.heads.stop
+            if self.units is None:
+                _check(lib.veda_tile_pool(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, _ptr(self.zq),
+                                          _ptr(self.cnt), _ptr(self.mask), s), "tile_pool(q)")
+                _check(lib.veda_tile_pool(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, _ptr(self.zk), None,
+                                          None, s), "tile_pool(k)")
+            else:  # the share's heads, on the whole call's padded grid
+                _check(lib.veda_tile_pool_heads(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, h0, h1,
+                                                _ptr(self.zq), _ptr(self.cnt), _ptr(self.mask), s), "tile_pool_heads(q)")
+                _check(lib.veda_tile_pool_heads(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, h0, h1,
+                                                _ptr(self.zk), None, None, s), "tile_pool_heads(k)")
             mark(1)
-            _check(lib.veda_tile_score_pooled(_ptr(self.zq), _ptr(self.zk), _ptr(self.cnt), Hh, NT, d,
-                                              ctypes.byref(self.scorer), _ptr(self.scores), _ptr(self.ws.buf),
-                                              self.ws.nbytes, s), "tile_score_pooled")
+            if h1 > h0:
+                _check(lib.veda_tile_score_pooled(_ptr(self.zq[h0:h1]), _ptr(self.zk[h0:h1]), _ptr(self.cnt[h0:h1]),
+                                                  h1 - h0, NT, d, ctypes.byref(self.scorer), _ptr(self.scores[h0:h1]),
+                                                  _ptr(self.ws.buf), self.ws.nbytes, s), "tile_score_pooled")
             mark(2)
-            _check(lib.veda_select_topk(_ptr(self.scores), Hh, NT, self.k, _ptr(self.idx), s), "select_topk")
+            if h1 > h0:
+                _check(lib.veda_select_topk(_ptr(self.scores[h0:h1]), h1 - h0, NT, self.k, _ptr(self.idx[h0:h1]), s),
+                       "select_topk")
             mark(3)
             if self.units is None:
                 _check(lib.veda_sparse_attn_fwd_tokens(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat, cfg,

@@ -176,3 +176,7 @@ def test_empty_inputs_rejected_before_device_work(lib):
     assert shape(lib.veda_tile_pool(fake, 16384, 128, lat, cfg, 0, 128, fake, fake, fake, None)) == "VEDA_ERR_SHAPE"
     assert shape(lib.veda_tile_pool(fake, 16384, 128, veda.Latent(4, 0, 8), cfg, 1, 128, fake, fake, fake,
                                     None)) == "VEDA_ERR_SHAPE"
+    assert shape(lib.veda_tile_pool_heads(fake, 16384, 128, lat, cfg, 1, 128, 0, 2, fake, fake, fake,
+                                          None)) == "VEDA_ERR_SHAPE"  # head range beyond Hh
+    assert shape(lib.veda_tile_pool_heads(fake, 16384, 128, lat, cfg, 1, 128, 1, 0, fake, fake, fake,
+                                          None)) == "VEDA_ERR_SHAPE"  # begin > end

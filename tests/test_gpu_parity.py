@@ -315,15 +315,16 @@ def test_end_to_end_path_object(V, oracle, mode):
 
 
 @pytest.mark.parametrize("G", [2, 3, 8])
-def test_path_object_unit_shares(V, G):
-    """Rank shares of the whole path (SparseAttention over the heads a unit share touches,
-    with units=...; what a rank runs under shard.unit_range) assemble to the single-GPU call
-    bit for bit: heads are independent, so a head subset's scores and lists are the full
-    call's rows.  (A head subset gets the padded grid of its own tile shapes; with one shape
-    for all heads, as in the bench presets, that is the full call's grid -- see DESIGN.md §7.)"""
+@pytest.mark.parametrize("uniform", [True, False])
+def test_path_object_unit_shares(V, G, uniform):
+    """Rank shares of the whole path (SparseAttention(units=shard.unit_range(...)): pooling on
+    the call's padded grid for the touched heads, their scores and lists, the share's
+    attention units) assemble to the single-GPU call bit for bit -- also with per-head tile
+    shapes, where a head subset's own grid would differ from the call's."""
     from paper_2605_30325_b200 import shard
 
-    c = Case("uniform5", lat=(9, 10, 13), cfgs=[(4, 4, 8)], d=128, Hh=5, sparsity=0.8)
+    cfgs = [(4, 4, 8)] if uniform else [(4, 4, 8), (8, 4, 4), (4, 8, 4), (8, 8, 2), (2, 8, 8)]
+    c = Case("units", lat=(9, 10, 13), cfgs=cfgs, d=128, Hh=5, sparsity=0.8)
     dev = torch.device("cuda")
     w = {n: t.to(dev) for n, t in c.w.items()}
     q, k, v = (t.to(dev) for t in (c.q, c.k, c.v))
@@ -333,13 +334,10 @@ def test_path_object_unit_shares(V, G):
     out = torch.full_like(q, 3.0)
     for r in range(G):
         u = shard.unit_range(c.Hh, NT, r, G)
-        hs = shard.heads_of_units(u, NT)
-        if len(hs) == 0:
-            continue
-        loc = (u.start - hs.start * NT, u.stop - hs.start * NT)
-        pr = V.SparseAttention(c.lat, c.cfgs[hs.start:hs.stop], len(hs), c.d,
-                               {n: t[hs.start:hs.stop] for n, t in w.items()}, k=full.k, units=loc)
-        pr(q[hs.start:hs.stop], k[hs.start:hs.stop], v[hs.start:hs.stop], out=out[hs.start:hs.stop])
+        pr = V.SparseAttention(c.lat, c.cfgs, c.Hh, c.d, w, sparsity=c.sparsity, units=(u.start, u.stop))
+        pr(q, k, v, out=out)
+        hs = pr.heads
+        assert torch.equal(pr.idx[hs.start:hs.stop], full.idx[hs.start:hs.stop])
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int16), want.view(torch.int16))
 

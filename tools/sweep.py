@@ -92,13 +92,9 @@ def main():
                         worst = 0.0
                         for rk in range(G):
                             u = shard.unit_range(heads, NT, rk, G)
-                            hs = shard.heads_of_units(u, NT)
-                            wr = {n: t[hs.start:hs.stop] for n, t in w.items()}
-                            loc = (u.start - hs.start * NT, u.stop - hs.start * NT)
-                            pr = veda.SparseAttention(lat, [pre.cfg], len(hs), 128, wr, sparsity=sp, device=dev,
-                                                      units=loc)
-                            sl = slice(hs.start, hs.stop)
-                            worst = max(worst, timeit(lambda: pr(q[sl], k[sl], v[sl], out=out[sl]), a.reps))
+                            pr = veda.SparseAttention(lat, [pre.cfg], heads, 128, w, sparsity=sp, device=dev,
+                                                      units=(u.start, u.stop))
+                            worst = max(worst, timeit(lambda: pr(q, k, v, out=out), a.reps))
                             del pr
                         r[f"rank_ms_G{G}_units"] = round(worst, 3)
             rows.append(r)
