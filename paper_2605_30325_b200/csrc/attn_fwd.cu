@@ -545,7 +545,7 @@ static veda_status launch_tok(const uint16_t *q, const uint16_t *k, const uint16
                               const int32_t *idx, const uint32_t *mask, int kk, float scale, uint16_t *o,
                               int64_t o_hs, int64_t o_ts, float *lse, int u_begin, int u_end, cudaStream_t stream)
 {
-    static TokParams tp;  // host staging (3-4 KB): filled per launch, passed by value
+    TokParams tp{};  // host staging (3-4 KB, per call: thread-safe), passed by value to the kernel
     CUtensorMap dummy;
     memset(&dummy, 0, sizeof dummy);
     const int MW = B / 32;
