@@ -39,6 +39,24 @@ def main():
         torch.cuda.synchronize()
         assert torch.equal(oh.view(torch.int16), o.cpu().view(torch.int16))
         print(f"{name}: ok (k={path.k}, n_tiles={path.shape.n_tiles})", flush=True)
+    # unit shares (veda_tile_pool_heads + veda_sparse_attn_fwd_tokens_units) with per-head
+    # tile shapes, shares split inside heads
+    from paper_2605_30325_b200 import shard
+    cfgs = [(4, 4, 8), (8, 4, 4), (4, 8, 4)]
+    pre = synth.Preset("units", (9, 10, 13), 3, 128, cfgs[0], 0.8)
+    q, k, v = (t.to(dev) for t in synth.qkv(pre, lat=(9, 10, 13), d=128))
+    w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, d=128, random_bias=True).items()}
+    full = veda.SparseAttention((9, 10, 13), cfgs, 3, 128, w, sparsity=0.8, device=dev)
+    want = full(q, k, v)
+    NT = full.shape.n_tiles
+    out = torch.zeros_like(q)
+    for r in range(3):
+        u = shard.unit_range(3, NT, r, 3)
+        veda.SparseAttention((9, 10, 13), cfgs, 3, 128, w, sparsity=0.8, device=dev, units=(u.start, u.stop))(
+            q, k, v, out=out)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), want.view(torch.int16))
+    print("unit shares: ok", flush=True)
     # scorer at a size where the GELU split's blocks loop over several row groups (R = 2 x 1000
     # rows, 500 row groups > the resident grid)
     pre = synth.Preset("scorer", (8, 16, 16), 2, 128, (4, 4, 8), 0.5)
