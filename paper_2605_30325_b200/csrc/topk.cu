@@ -140,7 +140,7 @@ __device__ __forceinline__ uint32_t count_ge(const uint32_t (&key)[C], uint32_t 
 }
 
 template <int C>
-__global__ void __launch_bounds__(TKW_WARPS * 32) topk_warp_kernel(const float *__restrict__ S, int rows, int NT,
+__global__ void __launch_bounds__(TKW_WARPS * 32, 3) topk_warp_kernel(const float *__restrict__ S, int rows, int NT,
                                                                    int k, int32_t *__restrict__ idx)
 {
     const int lane = threadIdx.x & 31;
