@@ -118,7 +118,7 @@ __device__ __forceinline__ double gelu_tab_g(double x)
 // in registers (J x 4 values per lane, K <= 128 J).  GELU: the row is the layer-1
 // pre-activation and the digits are those of GELU(x) (erf form, reading R8).
 template <typename T, int J, bool GELU, int WPR>
-__global__ void __launch_bounds__(256) split_rows_kernel(const T *__restrict__ X, int R, int K, int64_t sr,
+__global__ void __launch_bounds__(256, GELU ? 4 : 1) split_rows_kernel(const T *__restrict__ X, int R, int K, int64_t sr,
                                                          int64_t sb, int Kp, int batch, int8_t *__restrict__ out,
                                                          int32_t *__restrict__ ex)
 {
