@@ -272,24 +272,13 @@ constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 // combine the 5 accumulators exactly, scale, apply the epilogue op and store.
 template <int BN, int EPI>
 __device__ __forceinline__ void epi_tile(const GemmArgs &g, uint32_t tl, int b, int m0, int n0, int cbeg, int cend,
-                                         int row, uint32_t done_bar, uint32_t done_parity, uint32_t tfree_bar,
-                                         int *s_eb, double *s_col)
+                                         int row, int ea, uint32_t done_bar, uint32_t done_parity, uint32_t tfree_bar,
+                                         const int *s_eb, const double *s_col)
 {
-    // per-column data of this tile (exponent of B's row, bias / score factor) in smem
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");  // previous tile's readers done
-    for (int c = threadIdx.x - 64; c < BN; c += 32 * EPI_WARPS) {
-        const int n = n0 + c;
-        const bool ok = n < g.N;
-        s_eb[c] = ok ? __ldg(g.eb + (int64_t)b * g.N + n) : 0;
-        if (EPI == EPI_SCORE)
-            s_col[c] = (ok && __ldg(g.cnt + (int64_t)b * g.N + n) != 0) ? 1.0 / g.den : -INFINITY;
-        else
-            s_col[c] = ok ? (double)__ldg(g.bias + (int64_t)b * g.N + n) : 0.0;
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+    // s_eb / s_col: this tile's per-column data (exponent of B's row, bias / score factor),
+    // staged in shared memory by the caller one tile ahead; ea: this row's A exponent
     const int m = m0 + row;
     const bool mok = m < g.M;
-    const int ea = mok ? __ldg(g.ea + (int64_t)b * g.M + m) : 0;
     mbar_wait(done_bar, done_parity);
     tc_fence_after();
     const int64_t orow = ((int64_t)b * g.M + m) * g.N;
@@ -367,8 +356,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
 #define OZ_EMPTY(i) (sbar + 8u * (NSTAGE + (i)))
 #define OZ_DONE (sbar + 8u * (2 * NSTAGE))
 #define OZ_TFREE (sbar + 8u * (2 * NSTAGE + 1))
-    __shared__ int s_eb[BN];
-    __shared__ double s_col[BN];
+    __shared__ int s_eb[2][BN];  // per-column data of the current / next tile (epilogue)
+    __shared__ double s_col[2][BN];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nmb = (g.M + BM - 1) / BM, nnb = (g.N + BN - 1) / BN;
     const int ntiles = nmb * nnb * g.batch;
@@ -449,11 +438,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
         const int cbeg = ((warp - 2) >> 2) * (BN / 2), cend = cbeg + BN / 2;  // this warp's column half
         const int row = q * 32 + lane;
         const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
+        // per-column (and per-row) data of a tile is loaded into registers one tile ahead, so
+        // its global-load latency overlaps the previous tile's epilogue; staged to shared
+        // memory (double-buffered) behind one named barrier per tile
+        const int tid = threadIdx.x - 64;
+        int eb_r = 0, ea_r = 0;
+        double col_r = 0.0;
+        auto load_cols = [&](int t) {
+            int b, m0, n0;
+            tile_coords(t, b, m0, n0);
+            if (tid < BN) {
+                const int n = n0 + tid;
+                const bool ok = n < g.N;
+                eb_r = ok ? __ldg(g.eb + (int64_t)b * g.N + n) : 0;
+                if (EPI == EPI_SCORE)
+                    col_r = (ok && __ldg(g.cnt + (int64_t)b * g.N + n) != 0) ? 1.0 / g.den : -INFINITY;
+                else
+                    col_r = ok ? (double)__ldg(g.bias + (int64_t)b * g.N + n) : 0.0;
+            }
+            ea_r = (m0 + row < g.M) ? __ldg(g.ea + (int64_t)b * g.M + m0 + row) : 0;
+        };
+        if (blockIdx.x < ntiles) load_cols(blockIdx.x);
         int nt = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
             int b, m0, n0;
             tile_coords(t, b, m0, n0);
-            epi_tile<BN, EPI>(g, tl, b, m0, n0, cbeg, cend, row, OZ_DONE, (uint32_t)nt & 1u, OZ_TFREE, s_eb, s_col);
+            const int buf = nt & 1;  // last read two tiles ago: every warp passed the previous barrier
+            if (tid < BN) {
+                s_eb[buf][tid] = eb_r;
+                s_col[buf][tid] = col_r;
+            }
+            const int ea = ea_r;
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+            if (t + (int)gridDim.x < ntiles) load_cols(t + gridDim.x);
+            epi_tile<BN, EPI>(g, tl, b, m0, n0, cbeg, cend, row, ea, OZ_DONE, (uint32_t)nt & 1u, OZ_TFREE,
+                              s_eb[buf], s_col[buf]);
         }
     }
     tc_fence_before();
