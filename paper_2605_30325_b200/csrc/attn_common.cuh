@@ -1,7 +1,6 @@
-// attn_common.cuh -- pieces shared by the attention kernels of attn_fwd.cu (the default
-// two-slot schedule) and attn_fwd_alt.cu (the opt-in half-step and P-in-shared-memory
-// schedules): launch constants, kernel parameters, the token-layout tile decode and TMA
-// gather, the trace macro and the packed-fp32 softmax helpers.
+// attn_common.cuh -- pieces of the attention kernel (attn_fwd.cu): launch constants, kernel
+// parameters, the token-layout tile decode and TMA gather, the trace macro and the
+// packed-fp32 softmax helpers.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -179,12 +178,6 @@ __device__ __forceinline__ void fadd2_acc(float &s0, float &s1, float a, float b
 
 __device__ __forceinline__ float u2f(uint32_t u) { return __uint_as_float(u); }
 __device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
-
-// Opt-in schedules (attn_fwd_alt.cu), selected by VEDA_ATTN at library load:
-// which = 1 half-step ("hs"), 2 P in shared memory ("ps", B = d = 128 only).
-template <int B, int D, bool TOK>
-veda_status launch_alt(int which, const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv,
-                       const Params &p, const TokParams &tp, int units, cudaStream_t stream);
 
 }  // namespace attn
 }  // namespace veda

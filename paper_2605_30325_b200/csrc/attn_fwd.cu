@@ -480,22 +480,10 @@ static veda_status launch_kernel(const CUtensorMap &mq, const CUtensorMap &mk, c
                                  const TokParams &tp, int units, cudaStream_t stream)
 {
     using G = Geo<B, D>;
-    // opt-in schedules (attn_fwd_alt.cu): VEDA_ATTN=hs (half-step), VEDA_ATTN=ps (P in shared
-    // memory, B = d = 128 launches only)
-    static const int alt = [] {
-        const char *e = getenv("VEDA_ATTN");
-        if (e && e[0] == 'h' && e[1] == 's') return 1;
-        if (e && e[0] == 'p' && e[1] == 's') return 2;
-        return 0;
-    }();
-    if (alt == 1 || (alt == 2 && B == 128 && D == 128)) return launch_alt<B, D, TOK>(alt, mq, mk, mv, p, tp, units, stream);
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(sparse_attn_fwd_kernel<B, D, TOK>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-        if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-        attr_set = true;
-    }
+    // set per launch: the attribute belongs to the current device's context
+    cudaError_t e = cudaFuncSetAttribute(sparse_attn_fwd_kernel<B, D, TOK>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     int grid = (units + NSLOT - 1) / NSLOT;
     const int nsm = num_sms();
     if (grid > nsm) grid = nsm;
@@ -616,11 +604,6 @@ veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint1
                                const int32_t *idx, const uint32_t *mask, int Hh, int NT, int B, int d,
                                int kk, float scale, uint16_t *o, float *lse, cudaStream_t s)
 {
-    static const int sched = [] {
-        const char *e = getenv("VEDA_ATTN");
-        return (e && e[0] == '1' && e[1] == 'q') ? 1 : 0;
-    }();
-    if (sched == 1) return launch_sparse_attn_1q(q, k, v, idx, mask, Hh, NT, B, d, kk, scale, o, lse, s);
     if (B == 128 && d == 128) return attn::launch<128, 128>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
     if (B == 128 && d == 64) return attn::launch<128, 64>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
     if (B == 64 && d == 128) return attn::launch<64, 128>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);

@@ -82,9 +82,6 @@ veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *
 // true unless VEDA_SCORER=dmma (the FP64 tensor-core GEMMs of score.cu) is set at load;
 // scorers with a dimension above 1024 (split_rows holds a row in registers) use DMMA too
 bool scorer_uses_ozaki();
-veda_status launch_sparse_attn_1q(const uint16_t *q, const uint16_t *k, const uint16_t *v, const int32_t *idx,
-                                  const uint32_t *mask, int Hh, int NT, int B, int d, int kk, float scale,
-                                  uint16_t *o, float *lse, cudaStream_t s);
 veda_status launch_target_scores(const uint16_t *q, const uint16_t *k, const uint32_t *mask, const float *lse,
                                  int Hh, int NT, int B, int d, float scale, float *out, cudaStream_t s);
 veda_status launch_permute_scalar(const float *x, int64_t hs, const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp,

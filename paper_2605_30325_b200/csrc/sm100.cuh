@@ -102,6 +102,58 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
     }
 }
 
+// Non-suspending probe of one mbarrier phase (test_wait never sleeps, unlike try_wait).
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Spin on an mbarrier phase with test_wait (for latency-critical single-thread waiters);
+// traps after ~2^27 polls (a pipeline bug) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity)
+{
+    uint32_t spins = 0;
+    while (!mbar_test(bar, parity)) {
+        if (++spins == (1u << 27)) __trap();
+    }
+}
+// Wait on an mbarrier phase with a sleep between probes: for waiters that are off the
+// critical path (producer, loaders), so that their polling does not take issue slots from
+// the softmax warps sharing their SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns)
+{
+    uint32_t spins = 0;
+    while (!mbar_test(bar, parity)) {
+        __nanosleep(ns);
+        if (++spins == (1u << 26)) __trap();
+    }
+}
+// CTA-scope release store / acquire load of a shared-memory word (mailbox sequence numbers)
+__device__ __forceinline__ void st_release_shared(uint32_t addr, uint32_t v)
+{
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_shared(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+// three-input max (FMNMX3 on sm_100)
+__device__ __forceinline__ float fmax3f(float a, float b, float c)
+{
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void *tmap)
 {
@@ -136,6 +188,22 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const void *tmap, int3
         " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
         : "memory");
+}
+// L2 prefetch of a 5-D / 2-D tensor box (no shared-memory destination, no barrier)
+__device__ __forceinline__ void tma_prefetch_5d(const void *tmap, int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+                                                int32_t c4)
+{
+    asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const void *tmap, int32_t c0, int32_t c1)
+{
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const void *tmap, int32_t c0,
                                                  int32_t c1, uint32_t bar, uint64_t policy)
@@ -247,6 +315,153 @@ __device__ __forceinline__ void tc_commit_w(uint32_t bar)
         "elect.sync _|e, 0xffffffff;\n\t"
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
         : "memory");
+}
+
+// NK (4 or 8) back-to-back kind::f16 MMAs -- the K-steps of one 64- or 128-deep
+// contraction -- under ONE elect.sync.  Step kk uses A = a0 + kk*ASTEP, B = b0 + BOFF(kk)
+// with BOFF(kk) = (kk / 4) * BCH + (kk % 4) * BIN (descriptor units of 16 bytes, or TMEM
+// columns for a TMEM A operand).  Only step 0 takes `accumulate`; the rest accumulate.
+// One election per group keeps the issuing thread's per-MMA cost to two adds.
+// SS: A and B descriptors (shared memory); A steps like B with (ACH, AIN).
+template <int NK, uint32_t ACH, uint32_t AIN, uint32_t BCH, uint32_t BIN>
+__device__ __forceinline__ void mma_group_ss(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc,
+                                             uint32_t accumulate)
+{
+    static_assert(NK == 4 || NK == 8, "NK");
+#define VEDA_AO(k) ((k) / 4 * ACH + (k) % 4 * AIN)
+#define VEDA_BO(k) ((k) / 4 * BCH + (k) % 4 * BIN)
+    if constexpr (NK == 8) {
+        asm volatile(
+            "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "setp.eq.b32 t, %4, %4;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+            "add.s64 a, %1, %5;\n\tadd.s64 b, %2, %6;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+            "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+            "add.s64 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+            "add.s64 a, %1, %11;\n\tadd.s64 b, %2, %12;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+            "add.s64 a, %1, %13;\n\tadd.s64 b, %2, %14;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+            "add.s64 a, %1, %15;\n\tadd.s64 b, %2, %16;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+            "add.s64 a, %1, %17;\n\tadd.s64 b, %2, %18;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t}" ::"r"(d_tmem),
+            "l"(a0), "l"(b0), "r"(idesc), "r"(accumulate), "n"(VEDA_AO(1)), "n"(VEDA_BO(1)), "n"(VEDA_AO(2)),
+            "n"(VEDA_BO(2)), "n"(VEDA_AO(3)), "n"(VEDA_BO(3)), "n"(VEDA_AO(4)), "n"(VEDA_BO(4)), "n"(VEDA_AO(5)),
+            "n"(VEDA_BO(5)), "n"(VEDA_AO(6)), "n"(VEDA_BO(6)), "n"(VEDA_AO(7)), "n"(VEDA_BO(7))
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "setp.eq.b32 t, %4, %4;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+            "add.s64 a, %1, %5;\n\tadd.s64 b, %2, %6;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+            "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+            "add.s64 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t}" ::"r"(d_tmem),
+            "l"(a0), "l"(b0), "r"(idesc), "r"(accumulate), "n"(VEDA_AO(1)), "n"(VEDA_BO(1)), "n"(VEDA_AO(2)),
+            "n"(VEDA_BO(2)), "n"(VEDA_AO(3)), "n"(VEDA_BO(3))
+            : "memory");
+    }
+#undef VEDA_AO
+#undef VEDA_BO
+}
+// TS: A in TMEM (a0 = TMEM address, +ASTEP columns per step), B descriptor (shared memory).
+template <int NK, uint32_t ASTEP, uint32_t BSTEP>
+__device__ __forceinline__ void mma_group_ts(uint32_t d_tmem, uint32_t a0, uint64_t b0, uint32_t idesc,
+                                             uint32_t accumulate)
+{
+    static_assert(NK == 4 || NK == 8, "NK");
+    if constexpr (NK == 8) {
+        asm volatile(
+            "{\n\t.reg .pred e, p, t;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "setp.eq.b32 t, %4, %4;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+            "add.s32 a, %1, %5;\n\tadd.s64 b, %2, %6;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+            "add.s32 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+            "add.s32 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+            "add.s32 a, %1, %11;\n\tadd.s64 b, %2, %12;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+            "add.s32 a, %1, %13;\n\tadd.s64 b, %2, %14;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+            "add.s32 a, %1, %15;\n\tadd.s64 b, %2, %16;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+            "add.s32 a, %1, %17;\n\tadd.s64 b, %2, %18;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t}" ::"r"(d_tmem),
+            "r"(a0), "l"(b0), "r"(idesc), "r"(accumulate), "n"(ASTEP), "n"(BSTEP), "n"(2 * ASTEP), "n"(2 * BSTEP),
+            "n"(3 * ASTEP), "n"(3 * BSTEP), "n"(4 * ASTEP), "n"(4 * BSTEP), "n"(5 * ASTEP), "n"(5 * BSTEP),
+            "n"(6 * ASTEP), "n"(6 * BSTEP), "n"(7 * ASTEP), "n"(7 * BSTEP)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e, p, t;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "setp.eq.b32 t, %4, %4;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+            "add.s32 a, %1, %5;\n\tadd.s64 b, %2, %6;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+            "add.s32 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+            "add.s32 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t}" ::"r"(d_tmem),
+            "r"(a0), "l"(b0), "r"(idesc), "r"(accumulate), "n"(ASTEP), "n"(BSTEP), "n"(2 * ASTEP), "n"(2 * BSTEP),
+            "n"(3 * ASTEP), "n"(3 * BSTEP)
+            : "memory");
+    }
+}
+// Non-blocking probe of three mbarrier phases in one asm block (test_wait: latencies
+// overlap, the thread never suspends); bit i set iff barrier i's phase is complete.
+__device__ __forceinline__ uint32_t mbar_test3(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1, uint32_t b2,
+                                               uint32_t p2)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred q0, q1, q2;\n\t.reg .b32 t0, t1, t2;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q0, [%1], %2;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q1, [%3], %4;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q2, [%5], %6;\n\t"
+        "selp.u32 t0, 1, 0, q0;\n\t"
+        "selp.u32 t1, 2, 0, q1;\n\t"
+        "selp.u32 t2, 4, 0, q2;\n\t"
+        "or.b32 t0, t0, t1;\n\t"
+        "or.b32 %0, t0, t2;\n\t}"
+        : "=r"(ok)
+        : "r"(b0), "r"(p0), "r"(b1), "r"(p1), "r"(b2), "r"(p2)
+        : "memory");
+    return ok;
+}
+// 64-bit shared-memory mailbox word {value bits, sequence}: one naturally aligned 64-bit
+// access is single-copy atomic, so a reader that sees the expected sequence also sees the
+// value written with it -- no fence needed between writer and reader lanes.
+__device__ __forceinline__ void mbox_put(uint32_t addr, float v, uint32_t seq)
+{
+    const unsigned long long w = ((unsigned long long)seq << 32) | __float_as_uint(v);
+    asm volatile("st.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(addr), "l"(w) : "memory");
+}
+__device__ __forceinline__ float mbox_get(uint32_t addr, uint32_t seq)
+{
+    unsigned long long w;
+    uint32_t spins = 0;
+    do {
+        asm volatile("ld.relaxed.cta.shared::cta.b64 %0, [%1];" : "=l"(w) : "r"(addr) : "memory");
+        if (++spins == (1u << 27)) __trap();
+    } while ((uint32_t)(w >> 32) != seq);
+    return __uint_as_float((uint32_t)w);
 }
 
 // D[tmem] (+)= A[smem] . B[smem], kind::i8 (signed 8-bit A/B, s32 D, K = 32 per instruction);

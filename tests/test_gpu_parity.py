@@ -502,40 +502,6 @@ def test_full_size_sampled(V, oracle, preset, head_aware):
     assert torch.equal(V.tile_unpermute(qt, pre.lat, cfgs), q)
 
 
-def test_alt_schedule_1q_parity():
-    """The alternative one-query-tile schedule (csrc/attn_fwd_1q.cu, selected by VEDA_ATTN=1q
-    at library load) passes the same attention parity tests, in a fresh process."""
-    import os
-    import subprocess
-    import sys
-
-    here = os.path.dirname(os.path.abspath(__file__))
-    env = dict(os.environ, VEDA_ATTN="1q")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_parity.py"),
-                        "-k", "test_attention_vs_oracle or test_dense_k_equals_nt or test_random_lists_and_small_k or "
-                        "(test_end_to_end_path_object and tiled)"],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-
-
-@pytest.mark.parametrize("schedule", ["hs", "ps"])
-def test_alt_schedule_parity(schedule):
-    """The half-step schedule (sparse_attn_fwd_hs_kernel, VEDA_ATTN=hs) and the P-in-shared-
-    memory schedule (sparse_attn_fwd_ps_kernel, VEDA_ATTN=ps; B = d = 128 launches, the
-    others fall back to the default kernel) pass the attention parity tests of both
-    layouts, in a fresh process."""
-    import os
-    import subprocess
-    import sys
-
-    here = os.path.dirname(os.path.abspath(__file__))
-    env = dict(os.environ, VEDA_ATTN=schedule)
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_parity.py"),
-                        "-k", "test_attention_vs_oracle or test_dense_k_equals_nt or test_random_lists_and_small_k or "
-                        "test_end_to_end_path_object or tokens_equals_tiled or full_size_sampled or degenerate_latents"],
-                       env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-
 
 @pytest.mark.parametrize("NT,k", [(1, 1), (7, 3), (33, 32), (128, 5), (336, 34), (700, 36), (1920, 96),
                                   (2048, 2048), (2049, 100), (4880, 96)])
