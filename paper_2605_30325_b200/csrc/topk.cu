@@ -12,8 +12,6 @@
 // construction and identical to "sort by (S desc, j asc), take k, sort by j".
 #include "common.cuh"
 
-#include <cstdlib>
-#include <cstring>
 
 namespace veda {
 namespace {
@@ -184,6 +182,283 @@ __global__ void __launch_bounds__(TKW_WARPS * 32, 3) topk_warp_kernel(const floa
     }
 }
 
+
+// Candidate-filter select (the path's top-k for n_tiles <= 2048, one warp per row; same
+// contract and result as topk_warp_kernel).  The bitwise search above costs ~30 passes over
+// all keys of the row; here:
+//   1. the row is read with 16-byte loads (lane l holds scores 128m + 4l + e);
+//   2. a threshold T0 below the k-th largest score is guessed from the mean and deviation of
+//      a 128-score sample (a normal-quantile guess aiming at ~1.5k + 32 scores >= T0) and
+//      corrected by counting; one pass sets a per-lane 64-bit candidate mask (one compare and
+//      one bit-set per score);
+//   3. the k-th largest key is found among the candidates (~8 % of the row, re-read from L1)
+//      by interpolation search over the order-preserving keys (count of keys >= a probe),
+//      which ends on a probe with exactly k keys >= it or on a key whose ties straddle rank k.
+// Rows where no threshold works in a few tries (ties, few finite scores, k close to n_tiles)
+// run the full bitwise search.  The output goes through a bitmap over key-tile indices, so
+// it is ascending with ties resolved to the lower index.
+constexpr int TKF_WARPS = 8;
+constexpr int TKF_CL = 16;  // candidate keys per lane held in registers for the search
+
+// inverse of the standard normal upper tail, z with P(X > z) = p, 0 < p <= 0.5
+// (Abramowitz-Stegun 26.2.23, |error| < 4.5e-4 -- only a starting guess, corrected by counting)
+__device__ __forceinline__ float upper_quantile(float p)
+{
+    const float t = sqrtf(-2.f * __logf(p));
+    return t - (2.515517f + t * (0.802853f + t * 0.010328f)) / (1.f + t * (1.432788f + t * (0.189269f + t * 0.001308f)));
+}
+__device__ __forceinline__ float warp_sum(float v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+// k-th largest of the keys (per lane C of them) by the MSB-first bitwise search
+template <int C>
+__device__ __forceinline__ uint32_t kth_largest(const uint32_t (&key)[C], uint32_t kk)
+{
+    uint32_t T = 0;
+#pragma unroll 1
+    for (int b = 31; b >= 0; --b) {
+        const uint32_t c = T | (1u << b);
+        const uint32_t n = __reduce_add_sync(0xFFFFFFFFu, count_ge<C>(key, c));
+        if (n >= kk) {
+            T = c;
+            if (n == kk) break;
+        }
+    }
+    return T;
+}
+
+// V = float4 loads per lane (n_tiles <= 128 V <= 2048)
+template <int V>
+__global__ void __launch_bounds__(TKF_WARPS * 32, V >= 16 ? 2 : 3) topk_filter_kernel(const float *__restrict__ S,
+                                                                                       int rows, int NT, int k,
+                                                                                       int32_t *__restrict__ idx)
+{
+    static_assert(V <= 16, "64-bit candidate mask");
+    constexpr int NW = 4 * V;  // bitmap words: word i covers key tiles 32i .. 32i+31
+    __shared__ uint32_t s_gt[TKF_WARPS][NW], s_eq[TKF_WARPS][NW];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int row = blockIdx.x * TKF_WARPS + w;
+    if (row >= rows) return;
+    const float *s = S + (size_t)row * NT;
+    const bool vec = (NT & 3) == 0 && (reinterpret_cast<uintptr_t>(s) & 15u) == 0;
+    float x[4 * V];  // x[4m + e] = S[128m + 4 lane + e]
+#pragma unroll
+    for (int m = 0; m < V; ++m) {
+        const int j = 128 * m + 4 * lane;
+        if (vec && j + 3 < NT) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(s + j));
+            x[4 * m] = v.x; x[4 * m + 1] = v.y; x[4 * m + 2] = v.z; x[4 * m + 3] = v.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[4 * m + e] = j + e < NT ? __ldg(s + j + e) : -INFINITY;
+        }
+    }
+    const uint32_t kk = (uint32_t)k;
+    // threshold from a 128-score sample spread over the row (4 per lane, V/4 loads apart)
+    float sum = 0.f, sq = 0.f, nf = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float a = x[4 * (e * V / 4) + e];
+        if (isfinite(a)) { sum += a; sq = fmaf(a, a, sq); nf += 1.f; }
+    }
+    sum = warp_sum(sum);
+    sq = warp_sum(sq);
+    nf = warp_sum(nf);
+    bool ok = false;
+    float t0 = 0.f, mu = 0.f, sd = 0.f;
+    unsigned long long cm = 0;  // candidate mask: bit 4m + e
+    uint32_t c = 0;
+    if (nf >= 32.f && (float)k <= 0.2f * (float)NT) {
+        mu = sum / nf;
+        sd = sqrtf(fmaxf(sq / nf - mu * mu, 0.f));
+        float z = upper_quantile(fminf((1.5f * (float)k + 32.f) / (float)NT, 0.5f));
+#pragma unroll 1
+        for (int tries = 0; tries < 4 && sd > 0.f; ++tries) {
+            t0 = fmaf(z, sd, mu);
+            uint32_t lo32 = 0, hi32 = 0;
+#pragma unroll
+            for (int b = 0; b < 4 * V; ++b) {
+                if (b < 32)
+                    lo32 |= (x[b] >= t0 ? 1u : 0u) << b;
+                else
+                    hi32 |= (x[b] >= t0 ? 1u : 0u) << (b - 32);
+            }
+            cm = ((unsigned long long)hi32 << 32) | lo32;
+            const uint32_t nl = __popcll(cm);
+            c = __reduce_add_sync(0xFFFFFFFFu, nl);
+            const uint32_t nmax = __reduce_max_sync(0xFFFFFFFFu, nl);
+            if (c >= kk && nmax <= (uint32_t)TKF_CL) { ok = true; break; }
+            z += (c < kk) ? -0.5f : 0.3f;
+        }
+    }
+    uint32_t T;
+    if (ok) {
+        // candidate keys in registers (re-read from L1) with their key-tile indices
+        uint32_t key[TKF_CL];
+        uint16_t jj[TKF_CL];
+        unsigned long long mm = cm;
+#pragma unroll
+        for (int q = 0; q < TKF_CL; ++q) {
+            key[q] = 0u;
+            jj[q] = 0;
+            if (mm) {
+                const int b = __ffsll((long long)mm) - 1;
+                mm &= mm - 1;
+                const int j = 128 * (b >> 2) + 4 * lane + (b & 3);
+                jj[q] = (uint16_t)j;
+                key[q] = order_key(s[j]);
+            }
+        }
+        // interpolation search: count(>= lo) >= k > count(>= hi); the first probe comes from
+        // the normal model, the next ones alternate secant and bisection steps
+        uint32_t kmax = 0;
+#pragma unroll
+        for (int q = 0; q < TKF_CL; ++q) kmax = max(kmax, key[q]);
+        kmax = __reduce_max_sync(0xFFFFFFFFu, kmax);
+        uint32_t lo = order_key(t0), clo = c, chi = 0;
+        unsigned long long hi = (unsigned long long)kmax + 1ull;  // count(>= kmax + 1) = 0 < k
+        uint32_t guess = order_key(fmaf(upper_quantile(fminf(((float)k - 0.5f) / (float)NT, 0.5f)), sd, mu));
+        int step = 0;
+#pragma unroll 1
+        while (clo != kk && hi - lo > 1ull) {
+            const uint32_t span = (uint32_t)(hi - lo - 1ull);  // probes lie in (lo, hi)
+            uint32_t mid;
+            if (step == 0 && guess > lo && (unsigned long long)guess < hi) {
+                mid = guess;
+            } else {
+                uint32_t d = (step & 1) ? span / 2u + 1u
+                                        : (uint32_t)((float)span * ((float)(clo - kk) / (float)(clo - chi))) + 1u;
+                if (d > span) d = span;
+                mid = lo + d;
+            }
+            const uint32_t cmid = __reduce_add_sync(0xFFFFFFFFu, count_ge<TKF_CL>(key, mid));
+            if (cmid >= kk) { lo = mid; clo = cmid; } else { hi = mid; chi = cmid; }
+            ++step;
+            if (clo != kk && clo - chi <= 32u) {
+                // band finish: the <= 32 keys in [lo, hi) one per lane; the (k - chi)-th largest
+                // of them is the answer
+                uint32_t nb = 0;
+#pragma unroll
+                for (int q = 0; q < TKF_CL; ++q) nb += (key[q] >= lo && (unsigned long long)key[q] < hi) ? 1u : 0u;
+                uint32_t pb = nb;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, pb, o);
+                    if (lane >= o) pb += a;
+                }
+                pb -= nb;
+                __shared__ uint32_t s_band[TKF_WARPS][32];
+#pragma unroll
+                for (int q = 0; q < TKF_CL; ++q)
+                    if (key[q] >= lo && (unsigned long long)key[q] < hi) s_band[w][pb++] = key[q];
+                __syncwarp();
+                const uint32_t nbt = clo - chi, needb = kk - chi;
+                const uint32_t mine = (uint32_t)lane < nbt ? s_band[w][lane] : 0u;
+                uint32_t ngt_b = 0, nge_b = 0;
+#pragma unroll 8
+                for (int i2 = 0; i2 < 32; ++i2) {
+                    const uint32_t o = (uint32_t)i2 < nbt ? s_band[w][i2] : 0u;
+                    ngt_b += ((uint32_t)i2 < nbt && o > mine) ? 1u : 0u;
+                    nge_b += ((uint32_t)i2 < nbt && o >= mine) ? 1u : 0u;
+                }
+                const bool hit = (uint32_t)lane < nbt && ngt_b < needb && needb <= nge_b;
+                const uint32_t hb = __ballot_sync(0xFFFFFFFFu, hit);
+                lo = __shfl_sync(0xFFFFFFFFu, mine, __ffs(hb) - 1);
+                __syncwarp();
+                break;
+            }
+        }
+        // T = the k-th largest key: the smallest candidate key >= lo
+        uint32_t tmin = 0xFFFFFFFFu;
+#pragma unroll
+        for (int q = 0; q < TKF_CL; ++q)
+            if (key[q] >= lo) tmin = min(tmin, key[q]);
+        T = __reduce_min_sync(0xFFFFFFFFu, tmin);
+        // bitmaps of the candidates > T and == T
+#pragma unroll
+        for (int q = lane; q < NW; q += 32) { s_gt[w][q] = 0u; s_eq[w][q] = 0u; }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < TKF_CL; ++q)
+            if (key[q] >= T && key[q] != 0u) {
+                const uint32_t j = jj[q];
+                atomicOr(key[q] > T ? &s_gt[w][j >> 5] : &s_eq[w][j >> 5], 1u << (j & 31));
+            }
+    } else {
+        uint32_t key[4 * V];
+#pragma unroll
+        for (int b = 0; b < 4 * V; ++b) key[b] = 128 * (b >> 2) + 4 * lane + (b & 3) < NT ? order_key(x[b]) : 0u;
+        T = kth_largest<4 * V>(key, kk);
+#pragma unroll
+        for (int q = lane; q < NW; q += 32) { s_gt[w][q] = 0u; s_eq[w][q] = 0u; }
+        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < 4 * V; ++b)
+            if (key[b] >= T && key[b] != 0u) {
+                const uint32_t j = 128 * (b >> 2) + 4 * lane + (b & 3);
+                atomicOr(key[b] > T ? &s_gt[w][j >> 5] : &s_eq[w][j >> 5], 1u << (j & 31));
+            }
+    }
+    __syncwarp();
+    // ordered output: lane l owns bitmap words [l*WPL, (l+1)*WPL) (key tiles in index order)
+    constexpr int WPL = (NW + 31) / 32;
+    uint32_t gw[WPL], ew[WPL], ngt = 0, neq = 0;
+#pragma unroll
+    for (int q = 0; q < WPL; ++q) {
+        const int wi = lane * WPL + q;
+        gw[q] = wi < NW ? s_gt[w][wi] : 0u;
+        ew[q] = wi < NW ? s_eq[w][wi] : 0u;
+        ngt += __popc(gw[q]);
+        neq += __popc(ew[q]);
+    }
+    uint32_t gex = ngt, eex = neq;  // inclusive, then exclusive prefix sums over lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, gex, o), b = __shfl_up_sync(0xFFFFFFFFu, eex, o);
+        if (lane >= o) { gex += a; eex += b; }
+    }
+    gex -= ngt;
+    eex -= neq;
+    const uint32_t gt_total = __shfl_sync(0xFFFFFFFFu, gex + ngt, 31);
+    const uint32_t need = kk - gt_total;  // keys == T to take, lowest indices first
+    int take = (int)need - (int)eex;      // this lane's share of them
+#pragma unroll
+    for (int q = 0; q < WPL; ++q) {
+        uint32_t e = ew[q], kept = 0;
+        while (e && take > 0) {
+            const uint32_t bit = e & (0u - e);
+            kept |= bit;
+            e ^= bit;
+            --take;
+        }
+        gw[q] |= kept;
+    }
+    uint32_t nsel = 0;
+#pragma unroll
+    for (int q = 0; q < WPL; ++q) nsel += __popc(gw[q]);
+    uint32_t pos = nsel;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, pos, o);
+        if (lane >= o) pos += a;
+    }
+    pos -= nsel;
+    int32_t *out = idx + (size_t)row * k;
+#pragma unroll
+    for (int q = 0; q < WPL; ++q) {
+        uint32_t m = gw[q];
+        const int jb = (lane * WPL + q) * 32;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            out[pos++] = jb + b;
+        }
+    }
+}
+
 }  // namespace
 
 template <int C>
@@ -197,24 +472,23 @@ static veda_status launch_topk_warp(const float *scores, int rows, int NT, int k
 veda_status launch_topk(const float *scores, int Hh, int NT, int k, int32_t *idx, cudaStream_t s)
 {
     const int rows = Hh * NT;
-    static const bool force_cta = [] {
-        const char *e = getenv("VEDA_TOPK");
-        return e && !strcmp(e, "cta");
-    }();
-    if (!force_cta) {
-        if (NT <= 32 * 4) return launch_topk_warp<4>(scores, rows, NT, k, idx, s);
-        if (NT <= 32 * 16) return launch_topk_warp<16>(scores, rows, NT, k, idx, s);
-        if (NT <= 32 * 32) return launch_topk_warp<32>(scores, rows, NT, k, idx, s);
-        if (NT <= 32 * 64) return launch_topk_warp<64>(scores, rows, NT, k, idx, s);
+    if (NT <= 32 * 4) return launch_topk_warp<4>(scores, rows, NT, k, idx, s);
+    if (NT <= 32 * 64) {
+        const int grid = (rows + TKF_WARPS - 1) / TKF_WARPS;
+        if (NT <= 128 * 4)
+            topk_filter_kernel<4><<<grid, TKF_WARPS * 32, 0, s>>>(scores, rows, NT, k, idx);
+        else if (NT <= 128 * 8)
+            topk_filter_kernel<8><<<grid, TKF_WARPS * 32, 0, s>>>(scores, rows, NT, k, idx);
+        else
+            topk_filter_kernel<16><<<grid, TKF_WARPS * 32, 0, s>>>(scores, rows, NT, k, idx);
+        count_launch();
+        return check_launch("select_topk");
     }
     const size_t smem = (size_t)NT * sizeof(uint32_t);
     if (smem > 200 * 1024) return fail(VEDA_ERR_SHAPE, "select_topk: n_tiles=%d too large", NT);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+    if (smem > 48 * 1024) {  // per launch: the attribute belongs to the current device's context
+        cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-        attr = smem;
     }
     topk_kernel<<<rows, TK_THREADS, smem, s>>>(scores, NT, k, idx);
     count_launch();
