@@ -25,12 +25,14 @@
  *     validated before the first device call, so they report the same status with or
  *     without a GPU.  veda_last_error() gives a thread-local detail string for the
  *     last failure.  Faults inside a kernel surface later on the stream as CUDA errors.
- *   - Environment, read once at library load (measured alternatives, not the default
- *     path; profiles/r01_attn_experiments.md): VEDA_ATTN=hs|ps|1q selects another
- *     attention schedule (ps: B = d = 128 launches; 1q: tiled-layout calls only),
- *     VEDA_SCORER=dmma the FP64-tensor-core scorer instead of the INT8 Ozaki one
- *     (VEDA_GEMM=simt its CUDA-core GEMM), VEDA_TOPK=cta the CTA-per-row select.  Results agree within the tolerances tests/test_gpu_parity.py states
- *     (index lists and untiling bit-exact).
+ *   - Debug mode (veda_set_debug(1), or VEDA_DEBUG=1 in the environment at library
+ *     load): the attention, top-k and pooling entry points first validate their inputs
+ *     on the device -- kept-tile lists in [0, n_tiles) and strictly ascending (exactly k
+ *     distinct tiles; reading R11), bf16 inputs finite, scores not NaN
+ *     -- synchronise `stream`, and return VEDA_ERR_INDEX / VEDA_ERR_NONFINITE before
+ *     launching anything else.  Off by default (no validation, no synchronisation).
+ *     Whatever the mode, the attention kernels clamp every list entry into [0, n_tiles):
+ *     a bad list gives wrong outputs but never a read outside the head's tiles.
  *   - Supported: B = p_t*p_h*p_w in {64, 128}; d in {64, 128}; 1 <= k <= n_tiles;
  *     Hh <= 1024 heads per call.  Device must be sm_100 (B200).
  *
@@ -66,8 +68,8 @@ typedef enum {
     VEDA_ERR_K_RANGE = 4,    /* k outside [1, n_tiles]                            */
     VEDA_ERR_ALIGN = 5,      /* pointer or stride not 16-byte aligned             */
     VEDA_ERR_WORKSPACE = 6,  /* workspace too small                               */
-    VEDA_ERR_INDEX = 7,      /* (validation call) bad index list                  */
-    VEDA_ERR_NONFINITE = 8,  /* reserved                                          */
+    VEDA_ERR_INDEX = 7,      /* (debug mode) bad kept-tile list                    */
+    VEDA_ERR_NONFINITE = 8,  /* (debug mode) Inf/NaN input or NaN score            */
     VEDA_ERR_CUDA = 9,       /* CUDA runtime / driver error at launch             */
     VEDA_ERR_ARCH = 10       /* current device is not sm_100                      */
 } veda_status;
@@ -337,6 +339,28 @@ VEDA_API veda_status veda_tile_unpermute_scalar(const float *x_tiled, veda_laten
  * ACCUMULATED (zero it to start a calibration set).                                    */
 VEDA_API veda_status veda_sq_err(const uint16_t *a, const uint16_t *b, int64_t head_stride,
                         int64_t n, int32_t Hh, double *err, void *stream);
+
+/* ---- input validation (what debug mode runs) ---------------------- */
+
+/* bits OR-ed into the device flag word by the validation calls */
+#define VEDA_FLAG_INDEX_RANGE 1u  /* an entry outside [0, n_tiles)                        */
+#define VEDA_FLAG_INDEX_ORDER 2u  /* a row not strictly ascending: a duplicate or descent  */
+#define VEDA_FLAG_NONFINITE 4u    /* an Inf/NaN bf16 input, or a NaN score               */
+
+/* Kept-tile lists idx [rows][k] (as veda_select_topk writes them): ORs
+ * VEDA_FLAG_INDEX_RANGE / VEDA_FLAG_INDEX_ORDER into *flags (a DEVICE uint32 the caller
+ * zeroes; it is only ever OR-ed).  Enqueues and returns (no synchronisation).           */
+VEDA_API veda_status veda_validate_index(const int32_t *idx, int64_t rows, int32_t n_tiles, int32_t k,
+                                         uint32_t *flags, void *stream);
+
+/* bf16 token tensor x[h][n][c] (strides in elements, multiples of 8; d multiple of 8):
+ * ORs VEDA_FLAG_NONFINITE into *flags if any element is Inf or NaN.  A tiled tensor
+ * [Hh][N_T][B][d] is the case n = N_T*B, head_stride = n*d, token_stride = d.           */
+VEDA_API veda_status veda_validate_finite(const uint16_t *x, int64_t head_stride, int64_t token_stride,
+                                          int32_t Hh, int64_t n, int32_t d, uint32_t *flags, void *stream);
+
+/* Debug mode on (1) / off (0) for the whole process; returns the previous setting. */
+VEDA_API int32_t veda_set_debug(int32_t on);
 
 /* ---- diagnostics ------------------------------------------------------------------ */
 VEDA_API const char *veda_status_str(veda_status st);

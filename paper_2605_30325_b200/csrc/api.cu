@@ -163,14 +163,6 @@ veda_status shape_of(veda_latent lat, const veda_tile_cfg *cfg, int Hh, Shape *s
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
-bool scorer_uses_ozaki()
-{
-    static const bool oz = [] {
-        const char *e = getenv("VEDA_SCORER");
-        return !(e && strcmp(e, "dmma") == 0);
-    }();
-    return oz;
-}
 
 namespace {
 
@@ -208,6 +200,10 @@ veda_status veda_tile_score_workspace(int32_t Hh, int32_t n_tiles, int32_t d, co
     if (!w || !bytes) return fail(VEDA_ERR_NULL, "scorer or bytes is NULL");
     if (w->d_in != 3 * d) return fail(VEDA_ERR_SHAPE, "d_in=%d must equal 3*d=%d", w->d_in, 3 * d);
     if (Hh < 1 || n_tiles < 1 || w->d_hidden < 1 || w->d_lat < 1) return fail(VEDA_ERR_SHAPE, "bad sizes");
+    // the INT8 Ozaki scorer holds a row of each operand in registers
+    if (w->d_in > 1024 || w->d_hidden > 1024 || w->d_lat > 1024)
+        return fail(VEDA_ERR_SHAPE, "scorer dimensions (%d, %d, %d): each must be <= 1024", w->d_in, w->d_hidden,
+                    w->d_lat);
     const size_t rows = (size_t)Hh * n_tiles;
     size_t b = 0;
     b += 2 * align256(rows * w->d_in * sizeof(float));      // Zq, Zk
@@ -323,19 +319,10 @@ veda_status veda_tile_score(const uint16_t *q_tiled, const uint16_t *k_tiled, co
     double *ek = reinterpret_cast<double *>(p);
     if ((st = veda_trippool(q_tiled, slot_mask, Hh, n_tiles, B, d, zq, stream)) != VEDA_OK) return st;
     if ((st = veda_trippool(k_tiled, slot_mask, Hh, n_tiles, B, d, zk, stream)) != VEDA_OK) return st;
-    if (scorer_uses_ozaki() && w->d_in <= 1024 && w->d_hidden <= 1024 && w->d_lat <= 1024) {
-        const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
-        return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq,
-                                  ek, scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),
-                                  S(stream));
-    }
-    if ((st = veda_project(zq, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1q, w->b1q, w->w2q, w->b2q, hid, eq,
-                           stream)) != VEDA_OK)
-        return st;
-    if ((st = veda_project(zk, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1k, w->b1k, w->w2k, w->b2k, hid, ek,
-                           stream)) != VEDA_OK)
-        return st;
-    return veda_pair_scores(eq, ek, tile_count, Hh, n_tiles, w->d_lat, scores, stream);
+    const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
+    return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq, ek,
+                              scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),
+                              S(stream));
 }
 
 veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32_t *tile_count, int32_t Hh,
@@ -357,19 +344,10 @@ veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32
     double *hid = reinterpret_cast<double *>(p); p += align256(rows * w->d_hidden * sizeof(double));
     double *eq = reinterpret_cast<double *>(p); p += align256(rows * w->d_lat * sizeof(double));
     double *ek = reinterpret_cast<double *>(p);
-    if (scorer_uses_ozaki() && w->d_in <= 1024 && w->d_hidden <= 1024 && w->d_lat <= 1024) {
-        const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
-        return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq,
-                                  ek, scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),
-                                  S(stream));
-    }
-    if ((st = veda_project(zq, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1q, w->b1q, w->w2q, w->b2q, hid, eq,
-                           stream)) != VEDA_OK)
-        return st;
-    if ((st = veda_project(zk, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, w->w1k, w->b1k, w->w2k, w->b2k, hid, ek,
-                           stream)) != VEDA_OK)
-        return st;
-    return veda_pair_scores(eq, ek, tile_count, Hh, n_tiles, w->d_lat, scores, stream);
+    const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
+    return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq, ek,
+                              scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),
+                              S(stream));
 }
 
 veda_status veda_select_topk(const float *scores, int32_t Hh, int32_t n_tiles, int32_t k, int32_t *idx, void *stream)
@@ -379,6 +357,10 @@ veda_status veda_select_topk(const float *scores, int32_t Hh, int32_t n_tiles, i
     if (k < 1 || k > n_tiles) return fail(VEDA_ERR_K_RANGE, "select_topk: k=%d outside [1, %d]", k, n_tiles);
     veda_status st = check_arch();
     if (st != VEDA_OK) return st;
+    if (debug_mode() && (st = debug_validate(S(stream), [&](uint32_t *f) {
+                             return launch_validate_scores(scores, (int64_t)Hh * n_tiles * n_tiles, f, S(stream));
+                         })) != VEDA_OK)
+        return st;
     return launch_topk(scores, Hh, n_tiles, k, idx, S(stream));
 }
 
@@ -396,6 +378,17 @@ veda_status veda_sparse_attn_fwd(const uint16_t *q_tiled, const uint16_t *k_tile
         return fail(VEDA_ERR_ALIGN, "sparse_attn_fwd: tensors must be 16-byte aligned");
     veda_status st = check_arch();
     if (st != VEDA_OK) return st;
+    if (debug_mode()) {
+        const int64_t n = (int64_t)n_tiles * B;
+        st = debug_validate(S(stream), [&](uint32_t *f) {
+            veda_status e = launch_validate_index(idx, (int64_t)Hh * n_tiles, n_tiles, k, f, S(stream));
+            if (e == VEDA_OK) e = launch_validate_finite(q_tiled, n * d, d, Hh, n, d, f, S(stream));
+            if (e == VEDA_OK) e = launch_validate_finite(k_tiled, n * d, d, Hh, n, d, f, S(stream));
+            if (e == VEDA_OK) e = launch_validate_finite(v_tiled, n * d, d, Hh, n, d, f, S(stream));
+            return e;
+        });
+        if (st != VEDA_OK) return st;
+    }
     const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)d);
     return launch_sparse_attn(q_tiled, k_tiled, v_tiled, idx, slot_mask, Hh, n_tiles, B, d, k, scale, o_tiled, lse,
                               S(stream));
@@ -414,6 +407,11 @@ veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int64_t token
     veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // argument errors before any device call
     if (st != VEDA_OK) return st;
     if ((st = check_arch()) != VEDA_OK) return st;
+    if (debug_mode() && (st = debug_validate(S(stream), [&](uint32_t *f) {
+                             return launch_validate_finite(x, head_stride, token_stride, Hh,
+                                                           (int64_t)lat.t * lat.h * lat.w, d, f, S(stream));
+                         })) != VEDA_OK)
+        return st;
     return launch_tile_pool_tokens(x, head_stride, token_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
                                    sh.NT, d, z, tile_count, slot_mask, S(stream));
 }
@@ -434,6 +432,12 @@ veda_status veda_tile_pool_heads(const uint16_t *x, int64_t head_stride, int64_t
         return fail(VEDA_ERR_SHAPE, "tile_pool_heads: [%d, %d) outside [0, %d]", head_begin, head_end, Hh);
     if ((st = check_arch()) != VEDA_OK) return st;
     if (head_begin == head_end) return VEDA_OK;
+    if (debug_mode() && (st = debug_validate(S(stream), [&](uint32_t *f) {
+                             return launch_validate_finite(x + (size_t)head_begin * head_stride, head_stride,
+                                                           token_stride, head_end - head_begin,
+                                                           (int64_t)lat.t * lat.h * lat.w, d, f, S(stream));
+                         })) != VEDA_OK)
+        return st;
     HeadCfgs sub;
     const int hn = head_end - head_begin;
     for (int h = 0; h < hn; ++h) {
@@ -476,6 +480,17 @@ static veda_status sparse_attn_fwd_tokens_impl(const uint16_t *q, const uint16_t
     }
     if ((st = check_arch()) != VEDA_OK) return st;
     if (unit_begin == unit_end) return VEDA_OK;  // an empty share (e.g. a rank without units)
+    if (debug_mode()) {
+        const int64_t n = (int64_t)lat.t * lat.h * lat.w;
+        st = debug_validate(S(stream), [&](uint32_t *f) {
+            veda_status e = launch_validate_index(idx, (int64_t)n_units, sh.NT, k_keep, f, S(stream));
+            if (e == VEDA_OK) e = launch_validate_finite(q, head_stride, token_stride, Hh, n, d, f, S(stream));
+            if (e == VEDA_OK) e = launch_validate_finite(k, head_stride, token_stride, Hh, n, d, f, S(stream));
+            if (e == VEDA_OK) e = launch_validate_finite(v, head_stride, token_stride, Hh, n, d, f, S(stream));
+            return e;
+        });
+        if (st != VEDA_OK) return st;
+    }
     const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)d);
     return launch_sparse_attn_tok(q, k, v, head_stride, token_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w,
                                   sh.B, sh.NT, d, idx, slot_mask, k_keep, scale, o, o_head_stride, o_token_stride, lse,
@@ -596,5 +611,35 @@ const char *veda_last_error(void) { return g_err; }
 uint64_t veda_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 veda_status veda_check_device(void) { return check_arch(); }
+
+veda_status veda_validate_index(const int32_t *idx, int64_t rows, int32_t n_tiles, int32_t k, uint32_t *flags,
+                                void *stream)
+{
+    if (!idx || !flags) return fail(VEDA_ERR_NULL, "validate_index: NULL pointer");
+    if (rows < 0 || n_tiles < 1) return fail(VEDA_ERR_SHAPE, "validate_index: bad sizes");
+    if (k < 1 || k > n_tiles) return fail(VEDA_ERR_K_RANGE, "validate_index: k=%d outside [1, %d]", k, n_tiles);
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    return launch_validate_index(idx, rows, n_tiles, k, flags, S(stream));
+}
+
+veda_status veda_validate_finite(const uint16_t *x, int64_t head_stride, int64_t token_stride, int32_t Hh, int64_t n,
+                                 int32_t d, uint32_t *flags, void *stream)
+{
+    if (!x || !flags) return fail(VEDA_ERR_NULL, "validate_finite: NULL pointer");
+    if (Hh < 0 || n < 0 || d < 8 || (d % 8)) return fail(VEDA_ERR_SHAPE, "validate_finite: bad sizes");
+    if (!aligned16(x) || (head_stride % 8) || (token_stride % 8))
+        return fail(VEDA_ERR_ALIGN, "validate_finite: pointer/strides must be 16-byte aligned");
+    veda_status st = check_arch();
+    if (st != VEDA_OK) return st;
+    return launch_validate_finite(x, head_stride, token_stride, Hh, n, d, flags, S(stream));
+}
+
+int32_t veda_set_debug(int32_t on)
+{
+    const bool prev = debug_mode();
+    set_debug_mode(on != 0);
+    return prev ? 1 : 0;
+}
 
 }  // extern "C"

@@ -39,6 +39,10 @@ namespace veda {
 namespace attn {
 using namespace sm100;
 
+// A kept-tile list entry outside [0, n_tiles) (a caller bug; debug mode reports it as
+// VEDA_ERR_INDEX) is clamped, so the TMA coordinates and slot-mask reads stay inside the head.
+__device__ __forceinline__ int clamp_tile(int j, int NT) { return min(max(j, 0), NT - 1); }
+
 template <int B, int D>
 struct Geo {
     static constexpr int QCHUNK = 128 * 128;         // one 64-col chunk of the 128-row Q buffer
@@ -175,12 +179,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 };
 #pragma unroll
                 for (int s = 0; s < NSLOT; ++s)
-                    if (act[s]) { jv[s] = __ldg(il[s]); load_tile(&tmK, hh[s], jv[s]); }
+                    if (act[s]) { jv[s] = clamp_tile(__ldg(il[s]), NT); load_tile(&tmK, hh[s], jv[s]); }
                 for (int t = 0; t < K; ++t) {
 #pragma unroll
                     for (int s = 0; s < NSLOT; ++s) {
                         if (!act[s]) continue;
-                        const int jn = (t + 1 < K) ? __ldg(il[s] + t + 1) : 0;
+                        const int jn = (t + 1 < K) ? clamp_tile(__ldg(il[s] + t + 1), NT) : 0;
                         load_tile(&tmV, hh[s], jv[s]);
                         if (t + 1 < K) { jv[s] = jn; load_tile(&tmK, hh[s], jv[s]); }
                     }
@@ -330,12 +334,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int32_t *il = p.idx + (size_t)u * K;
             const uint32_t *mbase = p.slot_mask + (size_t)h * NT * G::MW;
             float m = -INFINITY, l = 0.f;
-            int jn = __ldg(il);
+            int jn = clamp_tile(__ldg(il), NT);
             for (int t = 0; t < K; ++t) {
                 uint32_t mk[G::MW];
 #pragma unroll
                 for (int w = 0; w < G::MW; ++w) mk[w] = __ldg(mbase + (size_t)jn * G::MW + w);
-                if (t + 1 < K) jn = __ldg(il + t + 1);
+                if (t + 1 < K) jn = clamp_tile(__ldg(il + t + 1), NT);
 
                 const int trs = r * K + t, trr = 1 + slot * 4 + quarter;  // trace role per softmax warp
                 if (lane == 0) TR(trr, trs, 0);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <functional>
 
 #include "../../include/veda.h"
 
@@ -79,9 +80,6 @@ size_t ozaki_workspace(int Hh, int NT, int din, int dh, int dl);
 veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *cnt, int Hh, int NT, int din, int dh,
                                int dl, const float *const w_q[4], const float *const w_k[4], double *hidden,
                                double *eq, double *ek, float *scores, void *scratch, cudaStream_t s);
-// true unless VEDA_SCORER=dmma (the FP64 tensor-core GEMMs of score.cu) is set at load;
-// scorers with a dimension above 1024 (split_rows holds a row in registers) use DMMA too
-bool scorer_uses_ozaki();
 veda_status launch_target_scores(const uint16_t *q, const uint16_t *k, const uint32_t *mask, const float *lse,
                                  int Hh, int NT, int B, int d, float scale, float *out, cudaStream_t s);
 veda_status launch_permute_scalar(const float *x, int64_t hs, const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp,
@@ -92,5 +90,17 @@ veda_status launch_sq_err(const uint16_t *a, const uint16_t *b, int64_t hs, int6
                           cudaStream_t s);
 veda_status launch_recall(const int32_t *sp, const int32_t *fu, const int32_t *cnt, int64_t rows, int NT, int k,
                           double *recall, cudaStream_t s);
+
+// input validation (validate.cu): kernels that OR VEDA_FLAG_* bits into a device word, and
+// debug mode (veda_set_debug / VEDA_DEBUG): run `enqueue(flags)`, synchronise, map flags to
+// VEDA_ERR_INDEX / VEDA_ERR_NONFINITE
+veda_status launch_validate_index(const int32_t *idx, int64_t rows, int n_tiles, int k, uint32_t *flags,
+                                  cudaStream_t s);
+veda_status launch_validate_finite(const uint16_t *x, int64_t hs, int64_t ts, int Hh, int64_t n, int d,
+                                   uint32_t *flags, cudaStream_t s);
+veda_status launch_validate_scores(const float *scores, int64_t n, uint32_t *flags, cudaStream_t s);
+bool debug_mode();
+void set_debug_mode(bool on);
+veda_status debug_validate(cudaStream_t s, const std::function<veda_status(uint32_t *)> &enqueue);
 
 }  // namespace veda

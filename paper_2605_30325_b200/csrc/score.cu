@@ -207,140 +207,12 @@ __global__ void __launch_bounds__(128) pool_tokens_kernel(const uint16_t *__rest
 
 // ---------------------------------------------------------------- fp64-accumulating GEMM
 // C[M,N] = A[M,K] . B  with B stored [K][N] (B_TRANS=false) or [N][K] (B_TRANS=true),
-// batched over blockIdx.z, operands widened to fp64 in shared memory, fp64 FMA.
-// 128x128 CTA tile, BK = 16, 256 threads, 8x8 outputs per thread laid out as 4x4 pairs
-// (rows qa*32 + ty*2 + {0,1}, cols qb*32 + tx*2 + {0,1}) so every shared-memory read is a
-// 16-byte, bank-conflict-free (or broadcast) load: 8 LDS.128 feed 64 DFMA per k.  The
-// next k-chunk is prefetched into registers while the current one is consumed.
+// batched over blockIdx.z, fp64 accumulation, with a fused epilogue.
 enum Epi { EPI_GELU_BIAS = 0, EPI_BIAS = 1, EPI_SCORE = 2 };
 
 constexpr int GB_M = 128, GB_N = 128, GB_K = 16;
 
-template <typename T>
-__device__ __forceinline__ void load8(const T *p, double (&v)[8], bool ok);
-template <>
-__device__ __forceinline__ void load8<float>(const float *p, double (&v)[8], bool ok)
-{
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-    if (ok) {
-        a = __ldg(reinterpret_cast<const float4 *>(p));
-        b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
-    }
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-}
-template <>
-__device__ __forceinline__ void load8<double>(const double *p, double (&v)[8], bool ok)
-{
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        double2 x = make_double2(0.0, 0.0);
-        if (ok) x = __ldg(reinterpret_cast<const double2 *>(p) + q);
-        v[2 * q] = x.x;
-        v[2 * q + 1] = x.y;
-    }
-}
-
-template <typename TA, typename TB, bool B_TRANS, int EPI>
-__global__ void __launch_bounds__(256, 1) gemm_f64acc_kernel(const TA *__restrict__ A,
-                                                             const TB *__restrict__ Bm,
-                                                             const float *__restrict__ bias,
-                                                             const int32_t *__restrict__ cnt, void *C,
-                                                             int M, int N, int K, int64_t sA, int64_t sB,
-                                                             int64_t sBias, int64_t sC, double den)
-{
-    __shared__ __align__(16) double As[GB_K][GB_M];
-    __shared__ __align__(16) double Bs[GB_K][GB_N];
-    const int z = blockIdx.z;
-    A += z * sA;
-    Bm += z * sB;
-    const int m0 = blockIdx.y * GB_M, n0 = blockIdx.x * GB_N;
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    // global->shared staging: A (and B^T) as 128 rows x 16 k, 8 consecutive k per thread;
-    // B as 16 k x 128 n, 8 consecutive n per thread
-    const int ar = tid >> 1, ak = (tid & 1) * 8;
-    const int bk = tid >> 4, bn = (tid & 15) * 8;
-    double ra[8], rb[8];
-    auto fetch = [&](int k0) {
-        const int gm = m0 + ar;
-        load8<TA>(A + (int64_t)gm * K + k0 + ak, ra, gm < M && k0 + ak < K);
-        if (!B_TRANS) {
-            const int gk = k0 + bk;
-            const bool ok = gk < K && n0 + bn < N;
-            if (ok && (N % 8) == 0 && n0 + bn + 8 <= N) {
-                load8<TB>(Bm + (int64_t)gk * N + n0 + bn, rb, true);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    rb[q] = (gk < K && n0 + bn + q < N) ? (double)Bm[(int64_t)gk * N + n0 + bn + q] : 0.0;
-            }
-        } else {
-            const int gn = n0 + ar;
-            load8<TB>(Bm + (int64_t)gn * K + k0 + ak, rb, gn < N && k0 + ak < K);
-        }
-    };
-    auto stash = [&]() {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) As[ak + q][ar] = ra[q];
-        if (!B_TRANS) {
-#pragma unroll
-            for (int q = 0; q < 8; q += 2) *reinterpret_cast<double2 *>(&Bs[bk][bn + q]) = make_double2(rb[q], rb[q + 1]);
-        } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) Bs[ak + q][ar] = rb[q];
-        }
-    };
-    double acc[8][8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-
-    fetch(0);
-    for (int k0 = 0; k0 < K; k0 += GB_K) {
-        stash();
-        __syncthreads();
-        if (k0 + GB_K < K) fetch(k0 + GB_K);  // next chunk in flight during the FMAs
-#pragma unroll
-        for (int kk = 0; kk < GB_K; ++kk) {
-            double a[8], b[8];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const double2 x = *reinterpret_cast<const double2 *>(&As[kk][q * 32 + ty * 2]);
-                const double2 y = *reinterpret_cast<const double2 *>(&Bs[kk][q * 32 + tx * 2]);
-                a[2 * q] = x.x; a[2 * q + 1] = x.y;
-                b[2 * q] = y.x; b[2 * q + 1] = y.y;
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int gm = m0 + (i >> 1) * 32 + ty * 2 + (i & 1);
-        if (gm >= M) continue;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int gn = n0 + (j >> 1) * 32 + tx * 2 + (j & 1);
-            if (gn >= N) continue;
-            const int64_t o = z * sC + (int64_t)gm * N + gn;
-            if (EPI == EPI_GELU_BIAS) {
-                const double x = acc[i][j] + (double)bias[z * sBias + gn];
-                static_cast<double *>(C)[o] = 0.5 * x * (1.0 + erf(x * 0.70710678118654752440));
-            } else if (EPI == EPI_BIAS) {
-                static_cast<double *>(C)[o] = acc[i][j] + (double)bias[z * sBias + gn];
-            } else {
-                const bool empty = cnt[z * (int64_t)N + gn] == 0;
-                static_cast<float *>(C)[o] = empty ? -INFINITY : (float)(acc[i][j] / den);
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------- fp64 tensor-core GEMM
-// Same contract as gemm_f64acc_kernel, on the FP64 tensor cores (DMMA,
+// The GEMM of veda_project / veda_pair_scores, on the FP64 tensor cores (DMMA,
 // mma.sync.m8n8k4.f64: exact fp64 products, fp64 accumulation).  128x128 CTA tile,
 // 8 warps as 2 (m) x 4 (n), warp tile 64x32 = 8x4 DMMA tiles, BK = 16 (4 k-steps).
 // Shared tiles are k-major with a 4-double row pad: fragment reads are conflict-free.
@@ -491,23 +363,8 @@ __global__ void __launch_bounds__(DM_THREADS, 1) gemm_dmma_kernel(const TA *__re
             }
 }
 
-bool use_dmma()
-{
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("VEDA_GEMM");
-        v = (e && e[0] == 's') ? 0 : 1;  // default: FP64 tensor cores
-    }
-    return v == 1;
-}
-
-#define VEDA_GEMM_LAUNCH(TA, TB, TR_, EPI_, grid, ...)                                         \
-    do {                                                                                      \
-        if (use_dmma())                                                                       \
-            gemm_dmma_kernel<TA, TB, TR_, EPI_><<<grid, DM_THREADS, 0, s>>>(__VA_ARGS__);     \
-        else                                                                                  \
-            gemm_f64acc_kernel<TA, TB, TR_, EPI_><<<grid, 256, 0, s>>>(__VA_ARGS__);          \
-    } while (0)
+#define VEDA_GEMM_LAUNCH(TA, TB, TR_, EPI_, grid, ...) \
+    gemm_dmma_kernel<TA, TB, TR_, EPI_><<<grid, DM_THREADS, 0, s>>>(__VA_ARGS__)
 
 }  // namespace
 

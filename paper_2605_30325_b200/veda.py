@@ -31,7 +31,7 @@ EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_worksp
            "veda_target_scores", "veda_tile_recall", "veda_tile_permute_scalar", "veda_tile_unpermute_scalar",
            "veda_sq_err", "veda_sparse_attention_host_workspace", "veda_sparse_attention_host",
            "veda_tile_pool", "veda_sparse_attn_fwd_tokens", "veda_sparse_attn_fwd_tokens_units",
-           "veda_tile_pool_heads"]
+           "veda_tile_pool_heads", "veda_validate_index", "veda_validate_finite", "veda_set_debug"]
 
 
 class VedaError(RuntimeError):
@@ -100,8 +100,13 @@ def load(path: str = LIB_PATH):
         "veda_last_error": ([], ctypes.c_char_p),
         "veda_launch_count": ([], ctypes.c_uint64),
         "veda_check_device": ([], i32),
+        "veda_validate_index": ([P, i64, i32, i32, P, P], i32),
+        "veda_validate_finite": ([P, i64, i64, i32, i64, i32, P, P], i32),
+        "veda_set_debug": ([i32], i32),
     }
     for name, (args, res) in sig.items():
+        if path != os.path.join(_HERE, "libveda.so") and not hasattr(lib, name):
+            continue  # an older library under VEDA_LIB (A/B timing): newer entry points absent
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
@@ -146,6 +151,35 @@ def launch_count() -> int:
 
 def check_device():
     _check(load().veda_check_device(), "check_device")
+
+
+FLAG_INDEX_RANGE, FLAG_INDEX_ORDER, FLAG_NONFINITE = 1, 2, 4
+
+
+def set_debug(on: bool) -> bool:
+    """Debug mode (include/veda.h): entry points validate their inputs and return
+    VEDA_ERR_INDEX / VEDA_ERR_NONFINITE.  Returns the previous setting."""
+    return bool(load().veda_set_debug(1 if on else 0))
+
+
+def validate_index(idx: torch.Tensor, n_tiles: int) -> int:
+    """VEDA_FLAG_* bits for kept-tile lists idx [..., k] (synchronises the current stream)."""
+    _need_cuda(idx)
+    k = idx.shape[-1]
+    flags = torch.zeros(1, dtype=torch.int32, device=idx.device)
+    _check(load().veda_validate_index(_ptr(idx), idx.numel() // k, n_tiles, k, _ptr(flags), _stream()),
+           "validate_index")
+    return int(flags.item())
+
+
+def validate_finite(x: torch.Tensor) -> int:
+    """VEDA_FLAG_NONFINITE if the bf16 tensor [Hh, N, d] (any strides, d contiguous) holds Inf/NaN."""
+    _need_cuda(x)
+    Hh, n, d = x.shape
+    flags = torch.zeros(1, dtype=torch.int32, device=x.device)
+    _check(load().veda_validate_finite(_ptr(x), x.stride(0), x.stride(1), Hh, n, d, _ptr(flags), _stream()),
+           "validate_finite")
+    return int(flags.item())
 
 
 @dataclass
@@ -583,14 +617,10 @@ class SparseAttention:
 
     @property
     def LAUNCHES_PER_CALL(self):
-        """Kernel launches of one call.  Scorer: INT8 Ozaki (default) = per side 2 x (split
-        rows, split cols, GEMM), then 2 splits + the score GEMM; the FP64 tensor-core path
-        (VEDA_SCORER=dmma, or a scorer dimension above 1024) = 2 x 2 phi layers + scores.
-        tokens: pool x2, scorer, topk, attn;  tiled: permute x3, pool x2, scorer, topk,
-        attn, unpermute."""
-        sc = self.scorer
-        ozaki = (os.environ.get("VEDA_SCORER") != "dmma" and max(sc.d_in, sc.d_hidden, sc.d_lat) <= 1024)
-        n = 15 if ozaki else 5
+        """Kernel launches of one call.  Scorer (INT8 Ozaki) = per side 2 x (split rows, split
+        cols, GEMM), then 2 splits + the score GEMM = 15.  tokens: pool x2, scorer, topk,
+        attn;  tiled: permute x3, pool x2, scorer, topk, attn, unpermute."""
+        n = 15
         return {"tokens": 2 + n + 1 + 1, "tiled": 3 + 2 + n + 1 + 1 + 1}
 
     def run_host(self, q, k, v, out=None, heads_per_chunk: int = 0):

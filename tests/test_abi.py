@@ -180,3 +180,19 @@ def test_empty_inputs_rejected_before_device_work(lib):
                                           None)) == "VEDA_ERR_SHAPE"  # head range beyond Hh
     assert shape(lib.veda_tile_pool_heads(fake, 16384, 128, lat, cfg, 1, 128, 1, 0, fake, fake, fake,
                                           None)) == "VEDA_ERR_SHAPE"  # begin > end
+
+
+def test_validation_calls_check_arguments_without_a_gpu(lib):
+    """veda_validate_index / veda_validate_finite reject bad arguments before any device call;
+    veda_set_debug toggles and reports the previous mode."""
+    from paper_2605_30325_b200 import veda
+
+    st = lib.veda_validate_index(None, 4, 8, 2, None, None)
+    assert veda.VEDA_STATUS[st] == "VEDA_ERR_NULL"
+    dummy = ctypes.c_void_p(16)
+    st = lib.veda_validate_index(dummy, 4, 8, 9, dummy, None)
+    assert veda.VEDA_STATUS[st] == "VEDA_ERR_K_RANGE"
+    st = lib.veda_validate_finite(dummy, 64, 8, 1, 8, 7, dummy, None)
+    assert veda.VEDA_STATUS[st] == "VEDA_ERR_SHAPE"
+    prev = lib.veda_set_debug(1)
+    assert lib.veda_set_debug(prev) == 1

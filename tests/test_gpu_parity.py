@@ -551,46 +551,40 @@ def test_host_pipeline_one_shot_api(V):
     assert torch.equal(got.view(torch.int16), want.view(torch.int16))
 
 
-_SCORER_SNIPPET = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, {root!r})
-from paper_2605_30325_b200 import synth, veda
-veda.load()
-pre = synth.PRESETS["waver12b"]
-dev = torch.device("cuda")
-heads = [0, 1, 2]
-q, k, v = synth.qkv(pre, heads=heads, device=dev)
-w = {{n: t.to(dev) for n, t in synth.scorer_weights(pre, heads=heads, random_bias=True).items()}}
-path = veda.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev)
-path(q, k, v)
-torch.cuda.synchronize()
-np.save({out!r}, path.scores.cpu().numpy())
-"""
+def test_scorer_int8_ozaki_vs_fp64_dmma(V):
+    """The path's INT8-tensor-core scorer (ozaki.cu, inside veda_tile_score_pooled) against the
+    FP64-tensor-core GEMMs of the exported per-stage calls veda_project + veda_pair_scores
+    (score.cu) on three full-size Waver heads: both are fp64-accurate, so the fp32 scores
+    agree to ~1 ulp (bound 2e-7 relative, far inside the 1e-5 near-tie window)."""
+    from paper_2605_30325_b200 import synth
 
-
-def test_scorer_int8_ozaki_vs_fp64_dmma(tmp_path):
-    """The INT8-tensor-core scorer (ozaki.cu, default) against the FP64-tensor-core scorer
-    (VEDA_SCORER=dmma) on three full-size Waver heads: both are fp64-accurate, so the fp32
-    scores agree to ~1 ulp (bound 2e-7 relative, far inside the 1e-5 near-tie window)."""
-    import os
-    import subprocess
-    import sys
-
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    outs = {}
-    for mode in ("ozaki", "dmma"):
-        out = str(tmp_path / f"s_{mode}.npy")
-        env = dict(os.environ, VEDA_SCORER=mode)
-        r = subprocess.run([sys.executable, "-c", _SCORER_SNIPPET.format(root=root, out=out)], env=env,
-                           capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0, r.stderr[-3000:]
-        outs[mode] = np.load(out)
-    a, b = outs["ozaki"], outs["dmma"]
+    pre = synth.PRESETS["waver12b"]
+    dev = torch.device("cuda")
+    heads = [0, 1, 2]
+    q, k, v = synth.qkv(pre, heads=heads, device=dev)
+    w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, heads=heads, random_bias=True).items()}
+    path = V.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev)
+    path(q, k, v)
+    eq = V.project(path.zq, w["w1q"], w["b1q"], w["w2q"], w["b2q"])
+    ek = V.project(path.zk, w["w1k"], w["b1k"], w["w2k"], w["b2k"])
+    b = V.pair_scores(eq, ek, path.cnt).cpu().numpy()
+    a = path.scores.cpu().numpy()
     assert np.array_equal(np.isfinite(a), np.isfinite(b))
     fin = np.isfinite(a)
     rel = np.abs(a[fin].astype(np.float64) - b[fin]) / np.maximum(1.0, np.abs(b[fin]))
     print(f"ozaki vs dmma: max rel {rel.max():.3e}, identical {np.mean(a[fin] == b[fin]) * 100:.2f} %")
     assert rel.max() < 2e-7
+
+
+def test_scorer_dimension_limit_is_an_error(V):
+    """Scorer dimensions above the INT8 scorer's limit are a shape error (no silent fallback)."""
+    from paper_2605_30325_b200 import synth
+
+    pre = synth.PRESETS["tiny"]
+    dev = torch.device("cuda")
+    w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, d_hidden=1040).items()}
+    with pytest.raises(V.VedaError, match="1024"):
+        V.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity, device=dev)
 
 
 @pytest.mark.parametrize("lat,cfg,d", [((1, 1, 1), (4, 4, 8), 128), ((1, 1, 1), (4, 4, 4), 64),
