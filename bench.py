@@ -46,7 +46,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-chunk", type=int, default=0,
                     help="heads per chunk of the host pipeline (0 = library default, ceil(Hh/32))")
-    ap.add_argument("--cpu-sample-units", type=int, default=24)
+    ap.add_argument("--cpu-sample-units", type=int, default=240,
+                    help="query tiles of one head the cpu_baseline times (240 = 1/8 of a Waver head)")
+    ap.add_argument("--ref-sample-units", type=int, default=48,
+                    help="query tiles per step of the --impl reference arm (a different sample each step)")
+    ap.add_argument("--ulysses-chunks", type=int, default=3,
+                    help="head chunks of the overlapped Ulysses exchange (N > 1)")
     return ap.parse_args()
 
 
@@ -116,10 +121,49 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_sample(pre, sparsity, n_units, seed_heads=(0,), seed=0):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_full(preset_name, sparsity=None):
+    """The fp64 oracle on a WHOLE call of a small workload (all heads, all query tiles)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2605_30325_b200 import synth
+
+    oracle.build()
+    pre = synth.PRESETS[preset_name]
+    sp = sparsity if sparsity is not None else pre.sparsity
+    q, k, v = synth.qkv(pre)
+    w = {n: t.numpy() for n, t in synth.scorer_weights(pre).items()}
+    u = lambda t: t.contiguous().view(torch.int16).numpy().view(np.uint16)
+    t0 = time.perf_counter()
+    oq, cnt, mask = oracle.tile_permute(u(q), pre.lat, [pre.cfg])
+    ok_, _, _ = oracle.tile_permute(u(k), pre.lat, [pre.cfg])
+    ov, _, _ = oracle.tile_permute(u(v), pre.lat, [pre.cfg])
+    eq = oracle.mlp(oracle.trippool(oq, mask), w["w1q"], w["b1q"], w["w2q"], w["b2q"])
+    ek = oracle.mlp(oracle.trippool(ok_, mask), w["w1k"], w["b1k"], w["w2k"], w["b2k"])
+    s = oracle.scores(eq, ek, cnt)
+    idx = oracle.topk(s.astype(np.float32).astype(np.float64), oracle.k_for_sparsity(s.shape[1], sp))
+    o = oracle.sparse_attn(oq, ok_, ov, idx, mask)
+    oracle.tile_unpermute(oracle.f64_to_bf16_bits(np.nan_to_num(o)), pre.lat, [pre.cfg])
+    return (time.perf_counter() - t0) * 1e3
+
+
+def oracle_sample(pre, sparsity, n_units, seed_heads=(0,), seed=0, single_thread_units=0):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload and
     extrapolate to one full call: steps a1-a5 and a7 on one head, attention (a6) on
-    ``n_units`` query tiles of that head.  Returns (ms_per_call, cores, sample)."""
+    ``n_units`` query tiles of that head (all host cores), plus optionally
+    ``single_thread_units`` more tiles on one thread.  Returns (ms_per_call, cores, sample,
+    wall_s, single_thread_ms_per_call or None)."""
     import numpy as np
     import torch
 
@@ -157,10 +201,19 @@ def oracle_sample(pre, sparsity, n_units, seed_heads=(0,), seed=0):
     per_head = (t1 - t0) + (t2 - t1) + (t3 - t2) + (t5 - t4)
     attn_per_unit = (t4 - t3) / len(units)
     total_s = pre.heads * (per_head + NT * attn_per_unit)
+    single = None
+    if single_thread_units > 0:
+        su = rng.choice(np.setdiff1d(np.arange(NT), units), size=min(single_thread_units, NT - len(units)),
+                        replace=False)
+        s0 = time.perf_counter()
+        oracle.sparse_attn(oq, ok_, ov, idx, mask, units=su.tolist(), nthreads=1)
+        st_unit = (time.perf_counter() - s0) / len(su)
+        single = pre.heads * (per_head + NT * st_unit) * 1e3
     sample = (f"oracle on 1 of {pre.heads} heads: tiling+scoring+top-k+untiling in full "
               f"({per_head:.1f} s), attention on {len(units)} of {NT} query tiles "
-              f"({t4 - t3:.1f} s, {cores} threads); extrapolated linearly to {pre.heads} heads x {NT} tiles")
-    return total_s * 1e3, cores, sample, t5 - t0
+              f"({t4 - t3:.1f} s, {cores} threads); extrapolated linearly (exact in work terms: every query "
+              f"tile does k tiles) to {pre.heads} heads x {NT} tiles")
+    return total_s * 1e3, cores, sample, time.perf_counter() - t0, single
 
 
 # ----------------------------------------------------------------------------- main arms
@@ -182,10 +235,10 @@ def run_reference(args):
     # sample per step) and extrapolates it to the whole call (exact in work terms: every
     # query tile does k tiles); warm-up steps are run and discarded
     for i in range(args.warmup):
-        oracle_sample(pre, sp, args.cpu_sample_units, seed=1000 + i)
+        oracle_sample(pre, sp, args.ref_sample_units, seed=1000 + i)
     vals, sample, cores = [], "", 0
     for i in range(args.steps):
-        v, cores, sample, _ = oracle_sample(pre, sp, args.cpu_sample_units, seed=i)
+        v, cores, sample, _, _ = oracle_sample(pre, sp, args.ref_sample_units, seed=i)
         vals.append(v)
     val = sum(vals) / len(vals)
     line = {"impl": "reference", "metric": METRIC, "value": round(val, 1), "unit": "ms", "n_gpus": args.gpus,
@@ -196,6 +249,7 @@ def run_reference(args):
                        "parallelism": f"heads{args.gpus}", "l2": "inputs larger than L2 (no flush)",
                        "regime": "path-produced lists"},
             "cpu_baseline": {"value": round(val, 1), "unit": "ms", "cores": cores, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"per step: {sample} (mean of {args.steps} steps)"},
             "e2e": {"value": round(val, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -360,7 +414,8 @@ def run_ours(args):
         ql, kl, vl = (t[t0:t0 + counts[rank]].contiguous() for t in (fq, fk, fv))
         del fq, fk, fv
         torch.cuda.empty_cache()
-        upath = uly.UlyssesSparseAttention(pre.lat, [pre.cfg], pre.heads, d, w, sparsity=sp, device=dev)
+        upath = uly.UlyssesSparseAttention(pre.lat, [pre.cfg], pre.heads, d, w, sparsity=sp, device=dev,
+                                           chunks=args.ulysses_chunks)
         for _ in range(args.warmup):
             upath(ql, kl, vl)
         barrier()
@@ -376,6 +431,10 @@ def run_ours(args):
     peaks = load_peaks()
     flops = 4.0 * B * B * d * kk * NT * Hh  # executed QK^T + PV FLOPs per launch (this rank)
     achieved = flops / (parts["attn"] * 1e-3) / 1e12
+    # HBM-bound steps: algorithmic bytes / time
+    n_tok = pre.lat[0] * pre.lat[1] * pre.lat[2]
+    pool_bytes = 2 * Hh * n_tok * d * 2 + 2 * Hh * NT * 3 * d * 4  # Q and K read once, Zq / Zk written
+    topk_bytes = Hh * NT * NT * 4 + Hh * NT * kk * 4                 # S read once, lists written
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(tp):
@@ -389,10 +448,15 @@ def run_ours(args):
     result = None
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            ms_cpu, cores, sample, wall = oracle_sample(pre, sp, args.cpu_sample_units)
-            cpu = {"value": round(ms_cpu, 1), "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample}
         clock = clk.summary()
+        if world == 1 and not args.no_cpu_baseline:
+            ms_cpu, cores, sample, wall, single = oracle_sample(pre, sp, args.cpu_sample_units,
+                                                                single_thread_units=8)
+            cpu = {"value": round(ms_cpu, 1), "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample,
+                   "cpu_model": cpu_model(), "single_thread_value": round(single, 1) if single else None,
+                   "full_call_tiny_ms": round(oracle_full("tiny"), 2),
+                   "full_calls_context": "profiles/r02_cpu_oracle.json (tools/cpu_oracle_bench.py: whole Wan-1.3B "
+                                         "and tiny calls, same host)"}
         result = {
             "metric": METRIC, "value": round(ms_step, 3), "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": False,
@@ -413,7 +477,21 @@ def run_ours(args):
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1),
                          "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
                          "frac": round(achieved / peaks["bf16_tflops_sustained"], 3), "traffic": traffic,
-                         "kernel": "sparse_attn_fwd", "peak_kind": f"bf16 dense sustained ({peaks['source']})"},
+                         "kernel": "sparse_attn_fwd", "peak_kind": f"bf16 dense sustained ({peaks['source']})",
+                         "peak_burst": peaks["bf16_tflops"],
+                         "frac_burst": round(achieved / peaks["bf16_tflops"], 3),
+                         # the tensor pipe's own rate at the clock this run held: 8192 bf16 FLOP per
+                         # clock per SM (128x128x16 MMA in 64 clk) x 148 SMs x the median SM clock
+                         "frac_of_clock_peak": (round(achieved / (8192 * 148 * clock["sm_mhz"] * 1e6 / 1e12), 3)
+                                                if clock.get("sm_mhz") else None),
+                         "sm_mhz": clock.get("sm_mhz")},
+            "hbm_steps": {"peak_gbs": peaks["hbm_gbs"],
+                          "pool": {"bytes": pool_bytes, "ms": round(parts["pool"], 3),
+                                   "gbs": round(pool_bytes / parts["pool"] / 1e6, 1),
+                                   "frac": round(pool_bytes / parts["pool"] / 1e6 / peaks["hbm_gbs"], 3)},
+                          "topk": {"bytes": topk_bytes, "ms": round(parts["topk"], 3),
+                                   "gbs": round(topk_bytes / parts["topk"] / 1e6, 1),
+                                   "frac": round(topk_bytes / parts["topk"] / 1e6 / peaks["hbm_gbs"], 3)}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

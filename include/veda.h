@@ -221,6 +221,25 @@ VEDA_API veda_status veda_sparse_attn_fwd_tokens_units(const uint16_t *q, const 
                                                        int64_t o_head_stride, int64_t o_token_stride, float *lse,
                                                        int32_t unit_begin, int32_t unit_end, void *stream);
 
+/* The heads [head_begin, head_end) of an Hh-head call, with every tensor holding THOSE heads
+ * only (head 0 of x / z / tile_count / slot_mask / q / k / v / idx / o / lse is global head
+ * head_begin): the sequence-parallel (Ulysses) rank's head shard.  cfg lists all Hh heads, so
+ * the padded grid, n_tiles and the tiles are the whole call's (with head-aware tiling a head
+ * subset's own grid can differ) and the results are bit-identical to the same heads of the
+ * whole call.  0 <= head_begin <= head_end <= Hh, else VEDA_ERR_SHAPE; an empty range enqueues
+ * nothing.  Other arguments as veda_tile_pool / veda_sparse_attn_fwd_tokens. */
+VEDA_API veda_status veda_tile_pool_local(const uint16_t *x, int64_t head_stride, int64_t token_stride,
+                                          veda_latent lat, const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh,
+                                          int32_t d, int32_t head_begin, int32_t head_end, float *z,
+                                          int32_t *tile_count, uint32_t *slot_mask, void *stream);
+VEDA_API veda_status veda_sparse_attn_fwd_tokens_local(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                                                       int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                                       const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh,
+                                                       int32_t d, int32_t head_begin, int32_t head_end,
+                                                       const int32_t *idx, const uint32_t *slot_mask, int32_t k_keep,
+                                                       float softmax_scale, uint16_t *o, int64_t o_head_stride,
+                                                       int64_t o_token_stride, float *lse, void *stream);
+
 /* ---- the whole path on HOST buffers (end-to-end call) ------------------------------ */
 
 /* Device workspace veda_sparse_attention_host needs (two buffer sets of one head chunk:

@@ -416,40 +416,59 @@ veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int64_t token
                                    sh.NT, d, z, tile_count, slot_mask, S(stream));
 }
 
-veda_status veda_tile_pool_heads(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
-                                 const veda_tile_cfg *cfg, int32_t Hh, int32_t d, int32_t head_begin,
-                                 int32_t head_end, float *z, int32_t *tile_count, uint32_t *slot_mask, void *stream)
+static veda_status tile_pool_range_impl(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                        const veda_tile_cfg *cfg, int32_t Hh, int32_t d, int32_t head_begin,
+                                        int32_t head_end, float *z, int32_t *tile_count, uint32_t *slot_mask,
+                                        bool local, void *stream)
 {
-    if (!x || !z) return fail(VEDA_ERR_NULL, "tile_pool_heads: NULL pointer");
+    const bool empty = head_begin == head_end && head_begin >= 0 && head_end <= Hh;
+    if ((!x || !z) && !(local && empty)) return fail(VEDA_ERR_NULL, "tile_pool_heads: NULL pointer");
     if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "tile_pool_heads: d=%d unsupported", d);
     if (!aligned16(x) || (head_stride % 8) || (token_stride % 8))
         return fail(VEDA_ERR_ALIGN, "tile_pool_heads: pointer/strides must be 16-byte aligned");
     Shape sh;
     HeadCfgs hc;
     veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // the whole call's padded grid
+    (void)empty;
     if (st != VEDA_OK) return st;
     if (head_begin < 0 || head_begin > head_end || head_end > Hh)
         return fail(VEDA_ERR_SHAPE, "tile_pool_heads: [%d, %d) outside [0, %d]", head_begin, head_end, Hh);
     if ((st = check_arch()) != VEDA_OK) return st;
     if (head_begin == head_end) return VEDA_OK;
+    // local: x and the outputs hold the range's heads only; else they are the whole call's
+    const size_t h0 = local ? 0 : (size_t)head_begin;
+    const int hn = head_end - head_begin;
     if (debug_mode() && (st = debug_validate(S(stream), [&](uint32_t *f) {
-                             return launch_validate_finite(x + (size_t)head_begin * head_stride, head_stride,
-                                                           token_stride, head_end - head_begin,
+                             return launch_validate_finite(x + h0 * head_stride, head_stride, token_stride, hn,
                                                            (int64_t)lat.t * lat.h * lat.w, d, f, S(stream));
                          })) != VEDA_OK)
         return st;
     HeadCfgs sub;
-    const int hn = head_end - head_begin;
     for (int h = 0; h < hn; ++h) {
         sub.pt[h] = hc.pt[head_begin + h];
         sub.ph[h] = hc.ph[head_begin + h];
         sub.pw[h] = hc.pw[head_begin + h];
     }
-    const size_t h0 = (size_t)head_begin;
     return launch_tile_pool_tokens(x + h0 * head_stride, head_stride, token_stride, sub, hn, sh.Tp, sh.Hp, sh.Wp, lat.t,
                                    lat.h, lat.w, sh.B, sh.NT, d, z + h0 * sh.NT * 3 * d,
                                    tile_count ? tile_count + h0 * sh.NT : nullptr,
                                    slot_mask ? slot_mask + h0 * sh.NT * (sh.B / 32) : nullptr, S(stream));
+}
+
+veda_status veda_tile_pool_heads(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                 const veda_tile_cfg *cfg, int32_t Hh, int32_t d, int32_t head_begin,
+                                 int32_t head_end, float *z, int32_t *tile_count, uint32_t *slot_mask, void *stream)
+{
+    return tile_pool_range_impl(x, head_stride, token_stride, lat, cfg, Hh, d, head_begin, head_end, z, tile_count,
+                                slot_mask, false, stream);
+}
+
+veda_status veda_tile_pool_local(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                 const veda_tile_cfg *cfg, int32_t Hh, int32_t d, int32_t head_begin,
+                                 int32_t head_end, float *z, int32_t *tile_count, uint32_t *slot_mask, void *stream)
+{
+    return tile_pool_range_impl(x, head_stride, token_stride, lat, cfg, Hh, d, head_begin, head_end, z, tile_count,
+                                slot_mask, true, stream);
 }
 
 static veda_status sparse_attn_fwd_tokens_impl(const uint16_t *q, const uint16_t *k, const uint16_t *v,
@@ -517,6 +536,54 @@ veda_status veda_sparse_attn_fwd_tokens_units(const uint16_t *q, const uint16_t 
     return sparse_attn_fwd_tokens_impl(q, k, v, head_stride, token_stride, lat, cfg, Hh, d, idx, slot_mask, k_keep,
                                        softmax_scale, o, o_head_stride, o_token_stride, lse, false, unit_begin,
                                        unit_end, stream);
+}
+
+veda_status veda_sparse_attn_fwd_tokens_local(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                                              int64_t head_stride, int64_t token_stride, veda_latent lat,
+                                              const veda_tile_cfg *cfg, int32_t Hh, int32_t d, int32_t head_begin,
+                                              int32_t head_end, const int32_t *idx, const uint32_t *slot_mask,
+                                              int32_t k_keep, float softmax_scale, uint16_t *o, int64_t o_head_stride,
+                                              int64_t o_token_stride, float *lse, void *stream)
+{
+    const bool empty = head_begin == head_end && head_begin >= 0 && head_end <= Hh;
+    if ((!q || !k || !v || !idx || !slot_mask || !o) && !empty)
+        return fail(VEDA_ERR_NULL, "sparse_attn_fwd_tokens_local: NULL pointer");
+    if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "sparse_attn_fwd_tokens_local: d=%d unsupported", d);
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || (head_stride % 8) || (token_stride % 8) ||
+        (o_head_stride % 8) || (o_token_stride % 8))
+        return fail(VEDA_ERR_ALIGN, "sparse_attn_fwd_tokens_local: pointers/strides must be 16-byte aligned");
+    Shape sh;
+    HeadCfgs hc;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // the whole call's padded grid
+    if (st != VEDA_OK) return st;
+    if (head_begin < 0 || head_begin > head_end || head_end > Hh)
+        return fail(VEDA_ERR_SHAPE, "sparse_attn_fwd_tokens_local: [%d, %d) outside [0, %d]", head_begin, head_end, Hh);
+    if (k_keep < 1 || k_keep > sh.NT)
+        return fail(VEDA_ERR_K_RANGE, "sparse_attn_fwd_tokens_local: k=%d outside [1, %d]", k_keep, sh.NT);
+    if ((st = check_arch()) != VEDA_OK) return st;
+    const int hn = head_end - head_begin;
+    if (hn == 0) return VEDA_OK;
+    if (debug_mode()) {
+        const int64_t n = (int64_t)lat.t * lat.h * lat.w;
+        st = debug_validate(S(stream), [&](uint32_t *f) {
+            veda_status e = launch_validate_index(idx, (int64_t)hn * sh.NT, sh.NT, k_keep, f, S(stream));
+            if (e == VEDA_OK) e = launch_validate_finite(q, head_stride, token_stride, hn, n, d, f, S(stream));
+            if (e == VEDA_OK) e = launch_validate_finite(k, head_stride, token_stride, hn, n, d, f, S(stream));
+            if (e == VEDA_OK) e = launch_validate_finite(v, head_stride, token_stride, hn, n, d, f, S(stream));
+            return e;
+        });
+        if (st != VEDA_OK) return st;
+    }
+    HeadCfgs sub;
+    for (int h = 0; h < hn; ++h) {
+        sub.pt[h] = hc.pt[head_begin + h];
+        sub.ph[h] = hc.ph[head_begin + h];
+        sub.pw[h] = hc.pw[head_begin + h];
+    }
+    const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)d);
+    return launch_sparse_attn_tok(q, k, v, head_stride, token_stride, sub, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w,
+                                  sh.B, sh.NT, d, idx, slot_mask, k_keep, scale, o, o_head_stride, o_token_stride, lse,
+                                  0, hn * sh.NT, S(stream));
 }
 
 veda_status veda_target_scores(const uint16_t *q_tiled, const uint16_t *k_tiled, const uint32_t *slot_mask,

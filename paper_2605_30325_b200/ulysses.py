@@ -41,6 +41,58 @@ def _restore(p: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
     return p.view(like.dtype) if like.element_size() == 2 else p
 
 
+def chunk_range(hr: range, c: int, C: int) -> range:
+    """Chunk c of C of a head range (sizes differ by at most one)."""
+    n = len(hr)
+    return range(hr.start + (c * n) // C, hr.start + ((c + 1) * n) // C)
+
+
+def seq_to_head_async(x_local: torch.Tensor, lat, heads_of, group=None):
+    """Start all-to-all #1 for the heads heads_of[j] of every rank j: returns (recv, work),
+    recv = this rank's heads [N, len(heads_of[rank]), d] once work.wait() returns (for NCCL:
+    once the current stream waits on it).  Rows arrive ordered by source rank = by token."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    Nr, Hh, d = x_local.shape
+    counts = token_counts(lat, world)
+    assert Nr == counts[rank], (Nr, counts)
+    send = torch.cat([_payload(x_local[:, hj.start:hj.stop, :]).reshape(-1) for hj in heads_of])
+    dp = d * x_local.element_size() // send.element_size()  # payload elements per row
+    my = heads_of[rank]
+    recv = torch.empty(sum(counts) * len(my) * dp, dtype=send.dtype, device=send.device)
+    work = dist.all_to_all_single(recv, send, output_split_sizes=[c * len(my) * dp for c in counts],
+                                  input_split_sizes=[Nr * len(hj) * dp for hj in heads_of], group=group,
+                                  async_op=True)
+    return _restore(recv.view(sum(counts), len(my), dp), x_local), work
+
+
+def head_to_seq_async(o_heads: torch.Tensor, lat, heads_of, group=None):
+    """Start all-to-all #2 of this rank's heads heads_of[rank] ([N, h, d]) back to the sequence
+    shards: returns (place, work); after work.wait(), place(out) writes the received rows into
+    out [N_r, Hh, d] (columns heads_of[j] of every source j)."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    N, Hr, d = o_heads.shape
+    counts = token_counts(lat, world)
+    assert Hr == len(heads_of[rank])
+    starts = [sum(counts[:i]) for i in range(world)]
+    send = torch.cat([_payload(o_heads[starts[i]:starts[i] + counts[i]]).reshape(-1) for i in range(world)])
+    dp = d * o_heads.element_size() // send.element_size()
+    Nr = counts[rank]
+    recv = torch.empty(Nr * sum(len(hj) for hj in heads_of) * dp, dtype=send.dtype, device=send.device)
+    work = dist.all_to_all_single(recv, send, output_split_sizes=[Nr * len(hj) * dp for hj in heads_of],
+                                  input_split_sizes=[c * Hr * dp for c in counts], group=group, async_op=True)
+
+    def place(out):
+        ov = _payload(out) if out.element_size() == 2 else out
+        ov = ov.view(Nr, -1, dp)
+        off = 0
+        for hj in heads_of:
+            n = Nr * len(hj) * dp
+            ov[:, hj.start:hj.stop, :] = recv[off:off + n].view(Nr, len(hj), dp)
+            off += n
+
+    return place, work
+
+
 def seq_to_head(x_local: torch.Tensor, lat, group=None) -> torch.Tensor:
     """[N_r, Hh, d] sequence shard -> [N, Hh_r, d] head shard (all-to-all #1)."""
     world, rank = dist.get_world_size(group), dist.get_rank(group)
@@ -85,23 +137,55 @@ class UlyssesSparseAttention:
 
     __call__(q, k, v) takes [N_r, Hh, d] bf16 CUDA tensors (this rank's frames, all heads)
     and returns o [N_r, Hh, d]; scorer_weights hold this rank's heads
-    (head_range(Hh, rank, G))."""
+    (head_range(Hh, rank, G)).  Every rank's head range is computed on the WHOLE call's
+    padded grid (SparseAttention(head_range=...)), so the output equals the single-GPU call
+    bit for bit, head-aware tiling included.
 
-    def __init__(self, lat, cfgs, Hh, d, scorer_weights, sparsity=None, k=None, group=None, device="cuda"):
+    chunks = C > 1 overlaps the exchange with the path: each rank's
+    heads are cut into C chunks; all 3C input all-to-alls (Q, K, V of each chunk) are started
+    at once, the path of chunk c runs as soon as its own three have landed -- while those of
+    chunks c+1.. are still in flight on the communicator's stream -- and the output
+    all-to-all of chunk c starts as soon as its path is done, overlapping chunk c+1's path."""
+
+    def __init__(self, lat, cfgs, Hh, d, scorer_weights, sparsity=None, k=None, group=None, device="cuda",
+                 chunks: int = 1):
         from . import veda
 
         self.lat, self.Hh, self.group = tuple(lat), Hh, group
         world, rank = dist.get_world_size(group), dist.get_rank(group)
+        self.world, self.rank = world, rank
         self.heads = head_range(Hh, rank, world)
+        self.chunks = max(1, int(chunks))
         cf = list(cfgs)
-        if len(cf) > 1:
-            cf = cf[self.heads.start:self.heads.stop]
-        self.path = veda.SparseAttention(lat, cf, len(self.heads), d, scorer_weights, sparsity=sparsity, k=k,
-                                         device=device)
+        if len(cf) == 1:
+            cf = cf * Hh
+        # the padded grid, N_T and k are the WHOLE call's (all Hh configs), so every rank's
+        # heads are computed exactly as in the single-GPU call even with head-aware tiling
+        self.paths = []
+        for c in range(self.chunks):
+            hc = chunk_range(self.heads, c, self.chunks)
+            a, b = hc.start - self.heads.start, hc.stop - self.heads.start
+            w = {n: t[a:b] for n, t in scorer_weights.items()}
+            self.paths.append(veda.SparseAttention(lat, cf, Hh, d, w, sparsity=sparsity, k=k, device=device,
+                                                   head_range=hc))
+        self.path = self.paths[0]
 
     def __call__(self, q, k, v):
-        qh, kh, vh = (seq_to_head(t, self.lat, self.group) for t in (q, k, v))  # [N, Hh_r, d]
-        o = torch.empty_like(qh)
-        # the path reads/writes [Hh_r, N, d] views of the [N, Hh_r, d] buffers (strided, no copy)
-        self.path(qh.transpose(0, 1), kh.transpose(0, 1), vh.transpose(0, 1), out=o.transpose(0, 1))
-        return head_to_seq(o, self.lat, self.Hh, self.group)
+        C, G = self.chunks, self.world
+        heads_of = [[chunk_range(head_range(self.Hh, j, G), c, C) for j in range(G)] for c in range(C)]
+        ins = [[seq_to_head_async(t, self.lat, heads_of[c], self.group) for t in (q, k, v)] for c in range(C)]
+        outs = []
+        for c in range(C):
+            for _, work in ins[c]:
+                work.wait()
+            qh, kh, vh = (r for r, _ in ins[c])  # [N, h_c, d]
+            o = torch.empty_like(qh)
+            if qh.shape[1]:
+                # the path reads/writes [h_c, N, d] views of the [N, h_c, d] buffers (strided, no copy)
+                self.paths[c](qh.transpose(0, 1), kh.transpose(0, 1), vh.transpose(0, 1), out=o.transpose(0, 1))
+            outs.append(head_to_seq_async(o, self.lat, heads_of[c], self.group))
+        out = torch.empty_like(q)
+        for place, work in outs:
+            work.wait()
+            place(out)
+        return out

@@ -31,7 +31,8 @@ EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_worksp
            "veda_target_scores", "veda_tile_recall", "veda_tile_permute_scalar", "veda_tile_unpermute_scalar",
            "veda_sq_err", "veda_sparse_attention_host_workspace", "veda_sparse_attention_host",
            "veda_tile_pool", "veda_sparse_attn_fwd_tokens", "veda_sparse_attn_fwd_tokens_units",
-           "veda_tile_pool_heads", "veda_validate_index", "veda_validate_finite", "veda_set_debug"]
+           "veda_tile_pool_heads", "veda_validate_index", "veda_validate_finite", "veda_set_debug",
+           "veda_tile_pool_local", "veda_sparse_attn_fwd_tokens_local"]
 
 
 class VedaError(RuntimeError):
@@ -103,6 +104,9 @@ def load(path: str = LIB_PATH):
         "veda_validate_index": ([P, i64, i32, i32, P, P], i32),
         "veda_validate_finite": ([P, i64, i64, i32, i64, i32, P, P], i32),
         "veda_set_debug": ([i32], i32),
+        "veda_tile_pool_local": ([P, i64, i64, Latent, P, i32, i32, i32, i32, P, P, P, P], i32),
+        "veda_sparse_attn_fwd_tokens_local": ([P, P, P, i64, i64, Latent, P, i32, i32, i32, i32, P, P, i32, f32, P,
+                                               i64, i64, P, P], i32),
     }
     for name, (args, res) in sig.items():
         if path != os.path.join(_HERE, "libveda.so") and not hasattr(lib, name):
@@ -490,17 +494,33 @@ class SparseAttention:
              "tiled": ("permute", "score", "topk", "attn", "unpermute")}
 
     def __init__(self, lat, cfgs, Hh, d, scorer_weights: dict, sparsity=None, k=None, device="cuda",
-                 mode="tokens", units=None):
+                 mode="tokens", units=None, head_range=None):
         """``units=(begin, end)`` (tokens mode): a rank's share under shard.unit_range of the
         flattened (head, query tile) units of this Hh-head call.  Pooling (on the call's
         padded grid, veda_tile_pool_heads), scoring and top-k then run for the heads the
         share touches only, and the attention for the share's units only
         (veda_sparse_attn_fwd_tokens_units); q, k, v, out stay the whole call's tensors and
-        only the share's output rows are written."""
+        only the share's output rows are written.
+
+        ``head_range=range(h0, h1)`` (tokens mode): this object computes the heads [h0, h1)
+        of an Hh-head call whose tile configs are ``cfgs`` (all Hh of them, so the padded
+        grid, N_T and k are the whole call's -- a head subset's own grid can differ with
+        head-aware tiling), but q, k, v, out and scorer_weights hold ONLY those heads
+        ([h1 - h0, N, d]; the Ulysses front end's head shards).  Outputs are bit-identical
+        to the same heads of the whole call."""
         if mode not in self.STEPS:
             raise VedaError(f"mode must be one of {list(self.STEPS)}")
-        if units is not None and mode != "tokens":
-            raise VedaError("units: tokens mode only")
+        if (units is not None or head_range is not None) and mode != "tokens":
+            raise VedaError("units / head_range: tokens mode only")
+        if units is not None and head_range is not None:
+            raise VedaError("units and head_range are exclusive")
+        self.head_range = None
+        if head_range is not None:
+            if not (0 <= head_range.start <= head_range.stop <= Hh):
+                raise VedaError(f"head_range {head_range} outside [0, {Hh}]")
+            self.head_range = head_range
+            NT0 = tiled_shape(lat, cfgs, Hh).n_tiles
+            units = (head_range.start * NT0, head_range.stop * NT0)
         self.units = None if units is None else (int(units[0]), int(units[1]))
         self.lat, self.cfgs, self.Hh, self.d, self.mode = tuple(lat), list(cfgs), Hh, d, mode
         self.shape = tiled_shape(lat, cfgs, Hh)
@@ -510,18 +530,23 @@ class SparseAttention:
         self.scorer = make_scorer(scorer_weights)
         dev = torch.device(device)
         self.device = dev
+        Hb = Hh if self.head_range is None else len(self.head_range)  # heads the buffers hold
         if mode == "tiled":
             mk = lambda: torch.empty((Hh, NT, B, d), dtype=torch.bfloat16, device=dev)
             self.qt, self.kt, self.vt, self.ot = mk(), mk(), mk(), mk()
         else:
-            self.zq = torch.empty((Hh, NT, 3 * d), dtype=torch.float32, device=dev)
-            self.zk = torch.empty((Hh, NT, 3 * d), dtype=torch.float32, device=dev)
-        self.cnt = torch.empty((Hh, NT), dtype=torch.int32, device=dev)
-        self.mask = torch.empty((Hh, NT, B // 32), dtype=torch.int32, device=dev)
-        self.scores = torch.empty((Hh, NT, NT), dtype=torch.float32, device=dev)
-        self.idx = torch.empty((Hh, NT, self.k), dtype=torch.int32, device=dev)
+            self.zq = torch.empty((Hb, NT, 3 * d), dtype=torch.float32, device=dev)
+            self.zk = torch.empty((Hb, NT, 3 * d), dtype=torch.float32, device=dev)
+        self.cnt = torch.empty((Hb, NT), dtype=torch.int32, device=dev)
+        self.mask = torch.empty((Hb, NT, B // 32), dtype=torch.int32, device=dev)
+        self.scores = torch.empty((Hb, NT, NT), dtype=torch.float32, device=dev)
+        self.idx = torch.empty((Hb, NT, self.k), dtype=torch.int32, device=dev)
         self.heads = range(Hh)
-        if self.units is not None:
+        if self.head_range is not None:
+            self.heads = self.head_range
+            if len(self.heads):
+                self.scorer = make_scorer(scorer_weights)
+        elif self.units is not None:
             from .shard import heads_of_units
 
             if not (0 <= self.units[0] <= self.units[1] <= Hh * NT):
@@ -546,7 +571,8 @@ class SparseAttention:
         cfg = _cfg_array(self.cfgs, Hh)
         NT, B = self.shape.n_tiles, self.shape.B
         if out is None:
-            out = torch.zeros((Hh, self.lat[0] * self.lat[1] * self.lat[2], d), dtype=torch.bfloat16,
+            Ho = Hh if self.head_range is None else len(self.head_range)
+            out = torch.zeros((Ho, self.lat[0] * self.lat[1] * self.lat[2], d), dtype=torch.bfloat16,
                               device=q.device)
         ev = events or [None] * 6
 
@@ -564,25 +590,38 @@ class SparseAttention:
                                           _ptr(self.cnt), _ptr(self.mask), s), "tile_pool(q)")
                 _check(lib.veda_tile_pool(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, _ptr(self.zk), None,
                                           None, s), "tile_pool(k)")
+            elif self.head_range is not None:  # head-shard tensors, the whole call's padded grid
+                _check(lib.veda_tile_pool_local(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, h0, h1,
+                                                _ptr(self.zq), _ptr(self.cnt), _ptr(self.mask), s), "tile_pool_local(q)")
+                _check(lib.veda_tile_pool_local(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, h0, h1,
+                                                _ptr(self.zk), None, None, s), "tile_pool_local(k)")
             else:  # the share's heads, on the whole call's padded grid
                 _check(lib.veda_tile_pool_heads(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, h0, h1,
                                                 _ptr(self.zq), _ptr(self.cnt), _ptr(self.mask), s), "tile_pool_heads(q)")
                 _check(lib.veda_tile_pool_heads(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, h0, h1,
                                                 _ptr(self.zk), None, None, s), "tile_pool_heads(k)")
             mark(1)
+            # score / top-k buffers: the whole call's rows (units) or the shard's own (head_range)
+            R = (lambda t, a, b: t[a:b]) if self.head_range is None else (lambda t, a, b: t)
             if h1 > h0:
-                _check(lib.veda_tile_score_pooled(_ptr(self.zq[h0:h1]), _ptr(self.zk[h0:h1]), _ptr(self.cnt[h0:h1]),
-                                                  h1 - h0, NT, d, ctypes.byref(self.scorer), _ptr(self.scores[h0:h1]),
-                                                  _ptr(self.ws.buf), self.ws.nbytes, s), "tile_score_pooled")
+                _check(lib.veda_tile_score_pooled(_ptr(R(self.zq, h0, h1)), _ptr(R(self.zk, h0, h1)),
+                                                  _ptr(R(self.cnt, h0, h1)), h1 - h0, NT, d, ctypes.byref(self.scorer),
+                                                  _ptr(R(self.scores, h0, h1)), _ptr(self.ws.buf), self.ws.nbytes, s),
+                       "tile_score_pooled")
             mark(2)
             if h1 > h0:
-                _check(lib.veda_select_topk(_ptr(self.scores[h0:h1]), h1 - h0, NT, self.k, _ptr(self.idx[h0:h1]), s),
-                       "select_topk")
+                _check(lib.veda_select_topk(_ptr(R(self.scores, h0, h1)), h1 - h0, NT, self.k,
+                                            _ptr(R(self.idx, h0, h1)), s), "select_topk")
             mark(3)
             if self.units is None:
                 _check(lib.veda_sparse_attn_fwd_tokens(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat, cfg,
                                                        Hh, d, _ptr(self.idx), _ptr(self.mask), self.k, 0.0, _ptr(out),
                                                        out.stride(0), out.stride(1), None, s), "sparse_attn_fwd_tokens")
+            elif self.head_range is not None:
+                _check(lib.veda_sparse_attn_fwd_tokens_local(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat,
+                                                             cfg, Hh, d, h0, h1, _ptr(self.idx), _ptr(self.mask),
+                                                             self.k, 0.0, _ptr(out), out.stride(0), out.stride(1),
+                                                             None, s), "sparse_attn_fwd_tokens_local")
             else:
                 _check(lib.veda_sparse_attn_fwd_tokens_units(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat,
                                                              cfg, Hh, d, _ptr(self.idx), _ptr(self.mask), self.k, 0.0,

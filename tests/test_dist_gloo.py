@@ -184,11 +184,26 @@ def _ulysses_worker(rank, world, port, out_dir):
     ok1 = torch.equal(xh.view(torch.int16), x[:, hr.start:hr.stop, :].contiguous().view(torch.int16))
     back = ulysses.head_to_seq(xh, ULAT, UHH)
     ok2 = torch.equal(back.view(torch.int16), x_local.view(torch.int16))
+    # chunked exchange (the overlapped front end's): chunk c of every rank's heads
+    ok3 = True
+    for C in (2, 3, 4):
+        heads_of = [[ulysses.chunk_range(head_range(UHH, j, world), c, C) for j in range(world)] for c in range(C)]
+        got = [ulysses.seq_to_head_async(x_local, ULAT, heads_of[c]) for c in range(C)]
+        out = torch.full_like(x_local, 7.0)
+        for c in range(C):
+            xc, w = got[c]
+            w.wait()
+            hc = heads_of[c][rank]
+            ok3 &= torch.equal(xc.view(torch.int16), x[:, hc.start:hc.stop, :].contiguous().view(torch.int16))
+            place, w2 = ulysses.head_to_seq_async(xc, ULAT, heads_of[c])
+            w2.wait()
+            place(out)
+        ok3 &= torch.equal(out.view(torch.int16), x_local.view(torch.int16))
     # full path on the head shard with the oracle as the kernel backend, then back to sequence
     res = _path_on_heads(xh, hr)
     o_seq = ulysses.head_to_seq(res, ULAT, UHH)
     np.save(os.path.join(out_dir, f"o{rank}.npy"), o_seq.view(torch.int16).numpy())
-    np.save(os.path.join(out_dir, f"ok{rank}.npy"), np.array([ok1, ok2]))
+    np.save(os.path.join(out_dir, f"ok{rank}.npy"), np.array([ok1, ok2, bool(ok3)]))
     dist.barrier()
     dist.destroy_process_group()
 

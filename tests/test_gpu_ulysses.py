@@ -20,8 +20,9 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("preset,head_aware", [("wan1.3b", False), ("wan1.3b", True)])
-def test_ulysses_nccl_world1_equals_direct(preset, head_aware):
+@pytest.mark.parametrize("preset,head_aware,chunks", [("wan1.3b", False, 1), ("wan1.3b", True, 1),
+                                                     ("wan1.3b", True, 3), ("wan1.3b", True, 16)])
+def test_ulysses_nccl_world1_equals_direct(preset, head_aware, chunks):
     from paper_2605_30325_b200 import build, synth, ulysses, veda
 
     build.build()
@@ -35,12 +36,48 @@ def test_ulysses_nccl_world1_equals_direct(preset, head_aware):
     try:
         w = {n: t.to(dev) for n, t in synth.scorer_weights(pre).items()}
         q, k, v = synth.qkv(pre, device=dev, layout="nhd")  # [N, Hh, d] sequence layout
-        up = ulysses.UlyssesSparseAttention(pre.lat, cfgs, pre.heads, pre.d, w, sparsity=pre.sparsity, device=dev)
+        up = ulysses.UlyssesSparseAttention(pre.lat, cfgs, pre.heads, pre.d, w, sparsity=pre.sparsity, device=dev,
+                                            chunks=chunks)
         o_u = up(q, k, v)
         path = veda.SparseAttention(pre.lat, cfgs, pre.heads, pre.d, w, sparsity=pre.sparsity, device=dev)
         o_d = path(q.transpose(0, 1), k.transpose(0, 1), v.transpose(0, 1))  # [Hh, N, d]
         torch.cuda.synchronize()
         assert torch.equal(o_u.view(torch.int16), o_d.transpose(0, 1).contiguous().view(torch.int16))
-        assert torch.equal(up.path.idx, path.idx)
+        if chunks == 1:
+            assert torch.equal(up.path.idx, path.idx)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("G", [2, 5, 8, 16])
+def test_head_range_shards_equal_single_gpu_call(G):
+    """What each Ulysses rank computes (SparseAttention(head_range=...) on its [N, Hh/G, d]
+    head shard, the exchange's output) assembles to the single-GPU call bit for bit with
+    head-aware per-head tile shapes -- the padded grid, N_T and k are the whole call's, not
+    those of the rank's own heads.  G = 16 > 12 heads leaves ranks without heads."""
+    from paper_2605_30325_b200 import build, shard, synth, veda
+
+    build.build()
+    veda.load()
+    pre = synth.PRESETS["wan1.3b"]
+    cfgs = [synth.HEAD_AWARE_CFGS[h % 4] for h in range(pre.heads)]
+    dev = torch.device("cuda", 0)
+    w = {n: t.to(dev) for n, t in synth.scorer_weights(pre).items()}
+    q, k, v = synth.qkv(pre, device=dev, layout="nhd")  # [N, Hh, d]
+    full = veda.SparseAttention(pre.lat, cfgs, pre.heads, pre.d, w, sparsity=pre.sparsity, device=dev)
+    want = full(q.transpose(0, 1), k.transpose(0, 1), v.transpose(0, 1))
+    got = torch.full_like(q, 3.0)
+    for r in range(G):
+        hr = shard.head_range(pre.heads, r, G)
+        wr = {n: t[hr.start:hr.stop] for n, t in w.items()}
+        qs, ks, vs = (t[:, hr.start:hr.stop].contiguous() for t in (q, k, v))  # the exchange's [N, Hh_r, d]
+        pr = veda.SparseAttention(pre.lat, cfgs, pre.heads, pre.d, wr, sparsity=pre.sparsity, device=dev,
+                                  head_range=hr)
+        assert pr.k == full.k and pr.shape.n_tiles == full.shape.n_tiles
+        o = torch.empty_like(qs)
+        pr(qs.transpose(0, 1), ks.transpose(0, 1), vs.transpose(0, 1), out=o.transpose(0, 1))
+        got[:, hr.start:hr.stop] = o
+        if len(hr):
+            assert torch.equal(pr.idx, full.idx[hr.start:hr.stop])
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int16), want.transpose(0, 1).contiguous().view(torch.int16))
