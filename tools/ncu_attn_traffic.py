@@ -29,7 +29,11 @@ def main():
     for r in rows[1:]:
         if "sparse_attn_fwd" not in r[h.index("Kernel Name")]:
             continue
-        vals[r[h.index("Metric Name")]] = (float(r[h.index("Metric Value")].replace(",", "")), r[h.index("Metric Unit")])
+        try:
+            vals[r[h.index("Metric Name")]] = (float(r[h.index("Metric Value")].replace(",", "")),
+                                               r[h.index("Metric Unit")])
+        except ValueError:
+            pass
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     rd = vals["dram__bytes_read.sum"]
     wr = vals["dram__bytes_write.sum"]
