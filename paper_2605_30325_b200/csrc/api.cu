@@ -83,7 +83,8 @@ veda_status make_tmap_bf16(CUtensorMap *map, const void *base, uint64_t rows, ui
 }
 
 veda_status make_tmap_tile_tokens(CUtensorMap *map, const void *base, int64_t head_stride, int64_t token_stride,
-                                  int Hh, int T, int H, int W, int d, int pt, int ph, int pw, int *tok_major)
+                                  int Hh, int T, int H, int W, int d, int pt, int ph, int pw, int *tok_major,
+                                  int box_c, bool swizzle)
 {
     auto fn = encode_fn();
     if (!fn) return fail(VEDA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -94,15 +95,15 @@ veda_status make_tmap_tile_tokens(CUtensorMap *map, const void *base, int64_t he
     if (!tm) {  // d, W, H, T, Hh
         dims[0] = d; dims[1] = W; dims[2] = H; dims[3] = T; dims[4] = Hh;
         strides[0] = ts; strides[1] = ts * W; strides[2] = ts * W * H; strides[3] = hs;
-        box[0] = 64; box[1] = pw; box[2] = ph; box[3] = pt; box[4] = 1;
+        box[0] = box_c; box[1] = pw; box[2] = ph; box[3] = pt; box[4] = 1;
     } else {    // d, Hh, W, H, T
         dims[0] = d; dims[1] = Hh; dims[2] = W; dims[3] = H; dims[4] = T;
         strides[0] = hs; strides[1] = ts; strides[2] = ts * W; strides[3] = ts * W * H;
-        box[0] = 64; box[1] = 1; box[2] = pw; box[3] = ph; box[4] = pt;
+        box[0] = box_c; box[1] = 1; box[2] = pw; box[3] = ph; box[4] = pt;
     }
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(base), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(VEDA_ERR_CUDA, "cuTensorMapEncodeTiled (5-D tile box) failed (%d)", (int)r);
     *tok_major = tm ? 1 : 0;
     return VEDA_OK;

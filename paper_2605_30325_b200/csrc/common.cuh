@@ -28,8 +28,11 @@ veda_status make_tmap_bf16(CUtensorMap *map, const void *base, uint64_t rows, ui
 // SWIZZLE_128B, out-of-grid slots zero-filled (reading R4) -- the same image as a 2-D box
 // of the tiled tensor.  Dimension order follows the strides (head-major: d,W,H,T,Hh;
 // token-major: d,Hh,W,H,T); *tok_major reports which.
+// box_c channels per box (64 with SWIZZLE_128B for the MMA operands; d without swizzle for
+// plain row-wise reads).
 veda_status make_tmap_tile_tokens(CUtensorMap *map, const void *base, int64_t head_stride, int64_t token_stride,
-                                  int Hh, int T, int H, int W, int d, int pt, int ph, int pw, int *tok_major);
+                                  int Hh, int T, int H, int W, int d, int pt, int ph, int pw, int *tok_major,
+                                  int box_c = 64, bool swizzle = true);
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

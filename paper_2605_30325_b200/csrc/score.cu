@@ -7,10 +7,10 @@
 //
 // Precision (R17): the kept index lists must match the fp64 oracle except at
 // near-ties < 1e-5, so every reduction here accumulates in fp64 (fp32 x fp32 products are
-// exact in fp64); scores are rounded once to fp32.  This file holds the pooling kernels
-// (tiled and token-layout) and the FP64-tensor-core (DMMA) GEMMs of phi / S_pred, used by
-// veda_project / veda_pair_scores and by veda_tile_score when VEDA_SCORER=dmma; the
-// default scorer GEMMs run on the INT8 tensor cores (ozaki.cu).
+// exact in fp64); scores are rounded once to fp32.  This file holds the pooling kernel of
+// the tiled form and the FP64-tensor-core (DMMA) GEMMs of phi / S_pred of the exported
+// per-stage calls veda_project / veda_pair_scores; the path's scorer GEMMs run on the INT8
+// tensor cores (ozaki.cu) and its pooling straight from token order in pool.cu.
 #include <cmath>
 #include <cstdlib>
 
@@ -97,110 +97,6 @@ __global__ void __launch_bounds__(128) trippool_kernel(const uint16_t *__restric
             zz[c] = (float)(s / (double)cnt);  // Avg: exact fp64 sum, one division, one rounding
             zz[D + c] = a;                      // Max
             zz[2 * D + c] = b;                  // Min
-        }
-    }
-}
-
-// ---------------------------------------------------------------- TripPool from tokens
-// The same descriptor (and tile_count / slot_mask) computed straight from the token
-// tensor: each CTA gathers its tile's rows from token order (box origin decoded once,
-// reading R1-R4) instead of reading a tiled copy -- one HBM pass over Q (or K) and no
-// permuted tensors at all.  Arithmetic identical to
-// trippool_kernel (fp64 sums in the same row order), so z is bit-identical.
-struct PoolGrid {
-    int T, H, W, Hp, Wp, NT;
-};
-
-template <int D, int BT>
-__global__ void __launch_bounds__(128) pool_tokens_kernel(const uint16_t *__restrict__ x, int64_t hs, int64_t ts,
-                                                          const __grid_constant__ HeadCfgs cf, const PoolGrid g,
-                                                          float *__restrict__ z, int32_t *__restrict__ cnt,
-                                                          uint32_t *__restrict__ mask)
-{
-    constexpr int CH = D / 8;
-    constexpr int RG = 128 / CH;
-    constexpr int RPT = BT / RG;
-    constexpr int MW = BT / 32;
-    const int ti = blockIdx.x;
-    const int h = ti / g.NT, i = ti - h * g.NT;
-    const int pt = cf.pt[h], ph = cf.ph[h], pw = cf.pw[h];
-    const int nbw = g.Wp / pw, nbh = g.Hp / ph;
-    const int it = i / (nbh * nbw), rem = i - it * nbh * nbw;
-    const int ih = rem / nbw, iw = rem - ih * nbw;
-    const int t0 = it * pt, h0 = ih * ph, w0 = iw * pw;
-    const int lpw = __ffs(pw) - 1, lphw = lpw + __ffs(ph) - 1;
-    const int c8 = threadIdx.x % CH, rg = threadIdx.x / CH;
-    const uint16_t *xh = x + (int64_t)h * hs;
-    uint4 v[RPT];
-    uint32_t valid = 0;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-        const int r = rg + q * RG;
-        const int t = t0 + (r >> lphw), hh = h0 + ((r >> lpw) & (ph - 1)), w = w0 + (r & (pw - 1));
-        const bool ok = t < g.T && hh < g.H && w < g.W;
-        valid |= (ok ? 1u : 0u) << q;
-        v[q] = ok ? __ldg(reinterpret_cast<const uint4 *>(xh + (((int64_t)t * g.H + hh) * g.W + w) * ts) + c8)
-                  : make_uint4(0, 0, 0, 0);
-    }
-    double sum[8];
-    float mx[8], mn[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) { sum[q] = 0.0; mx[q] = -INFINITY; mn[q] = INFINITY; }
-    int n = 0;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-        if (!((valid >> q) & 1u)) continue;
-        const uint32_t w[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
-            sum[2 * e] += (double)lo;
-            sum[2 * e + 1] += (double)hi;
-            mx[2 * e] = fmaxf(mx[2 * e], lo);
-            mx[2 * e + 1] = fmaxf(mx[2 * e + 1], hi);
-            mn[2 * e] = fminf(mn[2 * e], lo);
-            mn[2 * e + 1] = fminf(mn[2 * e + 1], hi);
-        }
-        ++n;
-    }
-    __shared__ double s_sum[RG][D];
-    __shared__ float s_mx[RG][D], s_mn[RG][D];
-    __shared__ int s_n[RG];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        s_sum[rg][c8 * 8 + q] = sum[q];
-        s_mx[rg][c8 * 8 + q] = mx[q];
-        s_mn[rg][c8 * 8 + q] = mn[q];
-    }
-    if (c8 == 0) s_n[rg] = n;
-    // slot mask: warp w < MW covers slots 32w .. 32w+31
-    if (threadIdx.x < MW * 32) {
-        const int r = threadIdx.x;
-        const int t = t0 + (r >> lphw), hh = h0 + ((r >> lpw) & (ph - 1)), w = w0 + (r & (pw - 1));
-        const uint32_t bits = __ballot_sync(0xFFFFFFFFu, t < g.T && hh < g.H && w < g.W);
-        if ((threadIdx.x & 31) == 0 && mask) mask[(int64_t)ti * MW + (r >> 5)] = bits;
-    }
-    __syncthreads();
-    float *zz = z + (size_t)ti * 3 * D;
-    int total = 0;
-#pragma unroll
-    for (int gq = 0; gq < RG; ++gq) total += s_n[gq];
-    if (threadIdx.x == 0 && cnt) cnt[ti] = total;
-    for (int c = threadIdx.x; c < D; c += 128) {
-        double sm = 0.0;
-        float a = -INFINITY, b = INFINITY;
-#pragma unroll
-        for (int gq = 0; gq < RG; ++gq) {
-            sm += s_sum[gq][c];
-            a = fmaxf(a, s_mx[gq][c]);
-            b = fminf(b, s_mn[gq][c]);
-        }
-        if (total == 0) {
-            zz[c] = 0.f; zz[D + c] = 0.f; zz[2 * D + c] = 0.f;
-        } else {
-            zz[c] = (float)(sm / (double)total);
-            zz[D + c] = a;
-            zz[2 * D + c] = b;
         }
     }
 }
@@ -384,28 +280,6 @@ veda_status launch_trippool(const uint16_t *xt, const uint32_t *mask, int Hh, in
         return fail(VEDA_ERR_SHAPE, "trippool: unsupported B=%d d=%d", B, d);
     count_launch();
     return check_launch("trippool");
-}
-
-veda_status launch_tile_pool_tokens(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfgs &cf, int Hh, int Tp,
-                                    int Hp, int Wp, int T, int H, int W, int B, int NT, int d, float *z,
-                                    int32_t *cnt, uint32_t *mask, cudaStream_t s)
-{
-    (void)Tp;
-    PoolGrid g;
-    g.T = T; g.H = H; g.W = W; g.Hp = Hp; g.Wp = Wp; g.NT = NT;
-    const int blocks = Hh * NT;
-    if (d == 128 && B == 128)
-        pool_tokens_kernel<128, 128><<<blocks, 128, 0, s>>>(x, hs, ts, cf, g, z, cnt, mask);
-    else if (d == 128 && B == 64)
-        pool_tokens_kernel<128, 64><<<blocks, 128, 0, s>>>(x, hs, ts, cf, g, z, cnt, mask);
-    else if (d == 64 && B == 128)
-        pool_tokens_kernel<64, 128><<<blocks, 128, 0, s>>>(x, hs, ts, cf, g, z, cnt, mask);
-    else if (d == 64 && B == 64)
-        pool_tokens_kernel<64, 64><<<blocks, 128, 0, s>>>(x, hs, ts, cf, g, z, cnt, mask);
-    else
-        return fail(VEDA_ERR_SHAPE, "tile_pool: unsupported B=%d d=%d", B, d);
-    count_launch();
-    return check_launch("tile_pool");
 }
 
 veda_status launch_project(const float *z, int Hh, int NT, int din, int dh, int dl, const float *w1,
