@@ -373,11 +373,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                 for (int c = 0; c < B / 32; ++c)
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) pm[i & 7] = fmaxf(pm[i & 7], u2f(sr[c][i]));
+                    for (int i = 0; i < 32; i += 2)  // three-input maxima (FMNMX3): half the instructions
+                        pm[(i >> 1) & 7] = fmax3f(pm[(i >> 1) & 7], u2f(sr[c][i]), u2f(sr[c][i + 1]));
                 const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                                        fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
                 const float mnew = fmaxf(m, mx * sl2);
-                if (lane == 0) TR(trr, trs, 3);
+                if (lane == 0 && mnew != 1.2345f) TR(trr, trs, 3);
                 // lazy rescale: only when some row of this warp grew its max by > 8 (log2 units)
                 float f = 1.f;
                 bool rescale = false;
