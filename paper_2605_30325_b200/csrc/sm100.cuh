@@ -146,6 +146,11 @@ __device__ __forceinline__ uint32_t ld_acquire_shared(uint32_t addr)
     asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
     return v;
 }
+// named barrier `id` (1..15) over `n` threads (a multiple of 32)
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 // three-input max (FMNMX3 on sm_100)
 __device__ __forceinline__ float fmax3f(float a, float b, float c)
 {

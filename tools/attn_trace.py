@@ -56,6 +56,10 @@ def main():
             r = t[1 + 4 * s, n]
             d = [r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4]]
             print(f"  t={n:3d} {r[0]:8d} {r[1]:8d} {r[2]:8d} {r[3]:8d} {r[4]:8d} {r[5]:8d} | " + " ".join(f"{x:6d}" for x in d))
+    for s in (0, 1):
+        for qq in range(4):
+            r = t[1 + 4 * s + qq, 1:a.steps]
+            print(f"slot {s} quarter {qq}: rescaled tiles {np.mean(r[:, 6] >= 0):.3f} (after the first)")
     # steady-state averages
     for s in (0, 1):
         r = t[1 + 4 * s, 4:a.steps]

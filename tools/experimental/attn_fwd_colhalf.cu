@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "attn_common.cuh"
 
@@ -42,6 +43,11 @@ using namespace sm100;
 // A kept-tile list entry outside [0, n_tiles) (a caller bug; debug mode reports it as
 // VEDA_ERR_INDEX) is clamped, so the TMA coordinates and slot-mask reads stay inside the head.
 __device__ __forceinline__ int clamp_tile(int j, int NT) { return min(max(j, 0), NT - 1); }
+
+// TMEM column (relative to the slot's S) of P's 16-key group g: the P of S chunk c (keys
+// [32c, 32c + 32), one softmax warp's) is stored over the first 16 of that chunk's own 32
+// columns, so no warp overwrites S another warp has still to read.
+__device__ __forceinline__ uint32_t p_col(int g) { return 32u * (g >> 1) + 8u * (g & 1); }
 
 template <int B, int D>
 struct Geo {
@@ -54,7 +60,9 @@ struct Geo {
     static constexpr int MW = B / 32;
     static constexpr int NPH = B / 64;                // P hand-off halves (64 keys each)
     static constexpr int NBAR = 2 * NST + (4 + NPH) * NSLOT;
-    static constexpr int SMEM = NSLOT * Q_BYTES + NST * TILE_BYTES + NBAR * 8 + 16 + 1024;
+    static constexpr int XCH = NSLOT * 2 * 128 * 4 + NSLOT * 2 * 4 * 4;  // row-sum exchange + S-loaded flags
+    // no alignment slack: the dynamic shared window starts 1024-aligned (checked at run time)
+    static constexpr int SMEM = NSLOT * Q_BYTES + NST * TILE_BYTES + NBAR * 8 + 16 + XCH;
     static_assert(NST >= 2, "ring too shallow");
 };
 
@@ -67,13 +75,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 {
     using G = Geo<B, D>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                                ~uintptr_t(1023));
+    uint8_t *smem = smem_raw;
+    if (smem_u32(smem_raw) & 1023u) __trap();  // SWIZZLE_128B operands need 1024-aligned stages
     const uint32_t sQ = smem_u32(smem);
     const uint32_t sRing = sQ + NSLOT * G::Q_BYTES;
     const uint32_t sBar = sRing + G::NST * G::TILE_BYTES;
     uint32_t *tmem_slot =
         reinterpret_cast<uint32_t *>(smem + NSLOT * G::Q_BYTES + G::NST * G::TILE_BYTES + G::NBAR * 8);
+    float *xch = reinterpret_cast<float *>(smem + NSLOT * G::Q_BYTES + G::NST * G::TILE_BYTES + G::NBAR * 8 + 16);
     // barrier addresses
 #define RING_FULL(i) (sBar + 8u * (i))
 #define RING_EMPTY(i) (sBar + 8u * (G::NST + (i)))
@@ -99,7 +108,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(Q_FULL(s), 1);
             mbar_init(Q_EMPTY(s), 1);
             mbar_init(S_FULL(s), 1);
-            for (int hf = 0; hf < G::NPH; ++hf) mbar_init(P_FULL(s, hf), 128);
+            for (int hf = 0; hf < G::NPH; ++hf) mbar_init(P_FULL(s, hf), 256);
             mbar_init(O_FULL(s), 1);
         }
         fence_barrier_init();
@@ -266,7 +275,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                 for (int k4 = 0; k4 < 4; ++k4) {
                     const int kk = hf * 4 + k4;
-                    mma_ts_w(tO, tP + kk * 8, vd0 + (uint64_t)((kk * 2048) >> 4), idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
+                    mma_ts_w(tO, tP + p_col(kk), vd0 + (uint64_t)((kk * 2048) >> 4), idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
                 }
                 if (t == K - 1 && hf == G::NPH - 1) tc_commit_w(O_FULL(s));
             };
@@ -308,7 +317,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         TR(0, npv, 4);
                         tc_fence_after();
                         // P arrives in two halves: the first half's PV runs while the softmax
-                        // still exponentiates the second (shortens the S -> P -> S chain per slot)
+                        // still computes the second (shortens the S -> P -> S chain per slot)
                         issue_pv(s, t, sv, 0);
                         if (G::NPH == 2) {
                             mbar_wait(P_FULL(s, 1), pp);
@@ -330,15 +339,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_SOFTMAX));
 #endif
         if (lane == 0) DBG("w%d softmax start\n", warp);
-        // ============================ softmax warpgroups ============================
-        const int slot = (warp - 4) >> 2;
+        // ============================ softmax warps ============================
+        // Warp 4 + 8*slot + 4*ch + quarter owns the rows of TMEM lane quarter `quarter`
+        // (= its SMSP) of slot `slot` and the S column chunks 2k + ch (32 keys each,
+        // k < B/64): two warps per SMSP share every tile, so the MUFU stream of a tile is
+        // fed by two warps (a single warp is scoreboard/latency-bound at ~20 clk per exp
+        // pair against 16 of MUFU).  The two halves of a row agree on the row max through
+        // shared memory and a 64-thread named barrier; chunk k of both warps is P hand-off k.
+        const int sw = warp - 4;
+        const int slot = sw >> 3, ch = (sw >> 2) & 1;
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         const uint32_t tS = tbase + lane_off + slot * 256;
-        const uint32_t tO = tS + 128;
+        const uint32_t tO = tS + 128 + ch * (D / 2);  // this warp's O columns
+        const uint32_t xbar = 1 + slot * 4 + quarter;  // named barrier of the warp pair
+        const uint32_t xmine = smem_u32(xch + (slot * 2 + ch) * 128 + row);
+        const uint32_t xpart = smem_u32(xch + (slot * 2 + (ch ^ 1)) * 128 + row);
+        // S-loaded flags: a warp's count of S tiles read out of TMEM (all four chunks)
+        uint32_t *const flags = reinterpret_cast<uint32_t *>(xch + NSLOT * 2 * 128);
+        const uint32_t fl_mine = smem_u32(flags + (slot * 2 + ch) * 4 + quarter);
+        const uint32_t fl_part = smem_u32(flags + (slot * 2 + (ch ^ 1)) * 4 + quarter);
+        uint32_t nld = 0;
         const float sl2 = p.scale_log2;
+        constexpr int NCW = B / 64;  // 32-key chunks per warp
         uint32_t sf_ph = 0, of_ph = 0;
+        if (lane == 0) st_shared_u32(fl_mine, 0u);
+        named_bar_sync(xbar, 64);
         for (int r = 0; r < rounds; ++r) {
             const int u = UNIT_OF(r, slot);
             if (u >= total) break;
@@ -348,55 +375,78 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             float m = -INFINITY, l = 0.f;
             int jn = clamp_tile(__ldg(il), NT);
             for (int t = 0; t < K; ++t) {
-                uint32_t mk[G::MW];
+                uint32_t mk[NCW], mkp[NCW];  // slot-mask words of this warp's / the partner's chunks
 #pragma unroll
-                for (int w = 0; w < G::MW; ++w) mk[w] = __ldg(mbase + (size_t)jn * G::MW + w);
+                for (int k = 0; k < NCW; ++k) {
+                    mk[k] = __ldg(mbase + (size_t)jn * G::MW + 2 * k + ch);
+                    mkp[k] = __ldg(mbase + (size_t)jn * G::MW + 2 * k + (ch ^ 1));
+                }
                 if (t + 1 < K) jn = clamp_tile(__ldg(il + t + 1), NT);
 
-                const int trs = r * K + t, trr = 1 + slot * 4 + quarter;  // trace role per softmax warp
-                if (lane == 0) TR(trr, trs, 0);
+                const int trs = r * K + t, trr = 1 + slot * 4 + quarter;  // trace role (ch 0 warps)
+                (void)trs; (void)trr;
+                if (lane == 0 && ch == 0) TR(trr, trs, 0);
                 mbar_wait(S_FULL(slot), sf_ph);
-                if (lane == 0) TR(trr, trs, 1);
+                if (lane == 0 && ch == 0) TR(trr, trs, 1);
                 sf_ph ^= 1;
-                if (lane == 0) DBG("w%d slot%d t%d S ok\n", warp, slot, t);
                 tc_fence_after();
-                uint32_t sr[B / 32][32];
-#pragma unroll
-                for (int c = 0; c < B / 32; ++c) tmem_ld32(tS + c * 32, sr[c]);
-                tmem_wait_ld();
-#pragma unroll
-                for (int c = 0; c < B / 32; ++c) reg_fence(sr[c]);
-                if (lane == 0) TR(trr, trs, 2);
-
-                bool full = true;
-#pragma unroll
-                for (int w = 0; w < G::MW; ++w) full &= (mk[w] == 0xFFFFFFFFu);
-                if (!full) {
-#pragma unroll
-                    for (int c = 0; c < B / 32; ++c)
-#pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (!((mk[c] >> i) & 1u)) sr[c][i] = f2u(-INFINITY);
-                }
-                // row max with 8 independent partial maxima (no 128-long dependency chain)
+                // Row max over all B keys, computed by each warp of the pair from TMEM (the
+                // partner's chunks first, then its own): no exchange and no barrier.  Own
+                // chunk 0 stays in registers; own chunk 1 is loaded again for its exp (the
+                // softmax warps live in 104 registers, and a spill would go to L2: shared
+                // memory takes the L1).
+                uint32_t s0[32];
                 float pm[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) pm[q] = -INFINITY;
+                auto fold = [&](const uint32_t(&s)[32]) {
 #pragma unroll
-                for (int c = 0; c < B / 32; ++c)
-#pragma unroll
-                    for (int i = 0; i < 32; i += 2)  // three-input maxima (FMNMX3): half the instructions
-                        pm[(i >> 1) & 7] = fmax3f(pm[(i >> 1) & 7], u2f(sr[c][i]), u2f(sr[c][i + 1]));
+                    for (int i = 0; i < 32; i += 4)
+                        pm[i >> 2] = fmax3f(pm[i >> 2], fmaxf(u2f(s[i]), u2f(s[i + 1])), fmaxf(u2f(s[i + 2]), u2f(s[i + 3])));
+                };
+                {
+                    uint32_t sa[32], sb[32];
+                    tmem_ld32(tS + 32 * (ch ^ 1), sa);
+                    if constexpr (NCW == 2) tmem_ld32(tS + 32 * (2 + (ch ^ 1)), sb);
+                    tmem_wait_ld();
+                    reg_fence(sa);
+                    if (mkp[0] != 0xFFFFFFFFu) mask_row(sa, mkp[0]);
+                    fold(sa);
+                    if constexpr (NCW == 2) {
+                        reg_fence(sb);
+                        if (mkp[1] != 0xFFFFFFFFu) mask_row(sb, mkp[1]);
+                        fold(sb);
+                    }
+                }
+                {
+                    uint32_t sb[32];
+                    tmem_ld32(tS + 32 * ch, s0);
+                    if constexpr (NCW == 2) tmem_ld32(tS + 32 * (2 + ch), sb);
+                    tmem_wait_ld();
+                    reg_fence(s0);
+                    ++nld;  // every column of this tile's S is in registers (or folded)
+                    __syncwarp();
+                    if (lane == 0) st_shared_u32(fl_mine, nld);
+                    if (lane == 0 && ch == 0) TR(trr, trs, 2);
+                    if (mk[0] != 0xFFFFFFFFu) mask_row(s0, mk[0]);
+                    fold(s0);
+                    if constexpr (NCW == 2) {
+                        reg_fence(sb);
+                        if (mk[1] != 0xFFFFFFFFu) mask_row(sb, mk[1]);
+                        fold(sb);
+                    }
+                }
                 const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                                        fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
                 const float mnew = fmaxf(m, mx * sl2);
-                if (lane == 0 && mnew != 1.2345f) TR(trr, trs, 3);
-                // lazy rescale: only when some row of this warp grew its max by > 8 (log2 units)
+                if (lane == 0 && ch == 0) TR(trr, trs, 3);
+                // lazy rescale: only when some row of this warp grew its max by > 8 (log2
+                // units); both warps of the pair see the same rows and maxima, so they agree
                 float f = 1.f;
                 bool rescale = false;
                 if (t == 0) {
                     m = mnew;
-                } else if (__any_sync(0xFFFFFFFFu, mnew > m + 8.0f)) {
+                } else if (__any_sync(0xFFFFFFFFu, mnew > m + HEADROOM)) {
                     f = (mnew == -INFINITY) ? 1.f : ex2(m - mnew);
                     rescale = true;
                     l *= f;
@@ -404,16 +454,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 const float mu = (m == -INFINITY) ? 0.f : m;
                 float ps[4] = {0.f, 0.f, 0.f, 0.f};
-                // P is handed to the MMA thread in halves of 64 keys (P_FULL(slot, half)):
-                // P V of the first half runs while the second half is exponentiated
+                auto exp_chunk = [&](const uint32_t (&s)[32], int k) {
+                    uint32_t pk[16];
 #pragma unroll
-                for (int c2 = 0; c2 < B / 64; ++c2) {
-                    uint32_t pk[32];
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const int c = 2 * c2 + (i >> 4), e = (i & 15) * 2;
+                    for (int i = 0; i < 16; ++i) {
                         float x0, x1;
-                        ffma2_bc(x0, x1, u2f(sr[c][e]), u2f(sr[c][e + 1]), sl2, -mu);
+                        ffma2_bc(x0, x1, u2f(s[2 * i]), u2f(s[2 * i + 1]), sl2, -mu);
                         float a, b;
                         if (EMU_EVERY > 0 && (i % EMU_EVERY) == EMU_EVERY - 1) {
                             ex2_emu2(a, b, x0, x1);  // FMA-pipe polynomial: unloads the MUFU unit
@@ -424,32 +470,52 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         fadd2_acc(ps[(i & 1) * 2], ps[(i & 1) * 2 + 1], a, b);
                         pk[i] = pack_bf16(a, b);
                     }
-                    tmem_st32(tS + c2 * 32, pk);  // P (bf16 pairs) over S columns already read
-                    if (c2 == 0 && rescale) {  // O is quiescent (see header); scale it before PV_t accumulates
+                    tmem_st16(tS + 32 * (2 * k + ch), pk);  // P (bf16 pairs) of keys [32(2k+ch), +32), over its own S
+                };
+                // P goes over S columns the partner also read (for its row max): wait until it
+                // has (normally long done: one shared-memory load)
+                while ((int)(ld_shared_u32(fl_part) - nld) < 0) { }
+                tc_fence_after();
+                exp_chunk(s0, 0);
+                if (rescale) {  // O is quiescent (see header): scale this warp's columns before PV_t
+#pragma unroll 1
+                    for (int c = 0; c < D / 64; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_wait_ld();
+                        reg_fence(o);
 #pragma unroll
-                        for (int c = 0; c < D / 32; ++c) {
-                            uint32_t o[32];
-                            tmem_ld32(tO + c * 32, o);
-                            tmem_wait_ld();
-                            reg_fence(o);
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * f);
-                            tmem_st32(tO + c * 32, o);
-                        }
+                        for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * f);
+                        tmem_st32(tO + c * 32, o);
                     }
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(P_FULL(slot, 0));
+                if (lane == 0 && ch == 0) TR(trr, trs, 4);
+                if constexpr (NCW == 2) {
+                    uint32_t s1[32];
+                    tmem_ld32(tS + 32 * (2 + ch), s1);
+                    tmem_wait_ld();
+                    reg_fence(s1);
+                    if (mk[1] != 0xFFFFFFFFu) mask_row(s1, mk[1]);
+                    exp_chunk(s1, 1);
                     tmem_wait_st();
                     tc_fence_before();
-                    mbar_arrive(P_FULL(slot, c2));
-                    if (lane == 0) TR(trr, trs, 4 + c2);
+                    mbar_arrive(P_FULL(slot, 1));
+                    if (lane == 0 && ch == 0) TR(trr, trs, 5);
                 }
                 l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
-                if (lane == 0 && rescale) TR(trr, trs, 6);
-                if (lane == 0) DBG("w%d slot%d t%d P arrive l=%f m=%f\n", warp, slot, t, l, m);
+                if (lane == 0 && ch == 0 && rescale) TR(trr, trs, 6);
             }
-            // ---- epilogue: O / l -> bf16, padded query rows -> 0
+            // ---- epilogue: O / l -> bf16 (this warp's D/2 columns), padded query rows -> 0
             mbar_wait(O_FULL(slot), of_ph);
             of_ph ^= 1;
             tc_fence_after();
+            st_shared_f32(xmine, l);  // row sum of the two halves (same reference m in both warps)
+            named_bar_sync(xbar, 64);
+            l += ld_shared_f32(xpart);
+            named_bar_sync(xbar, 64);  // both read before either writes the next row max
             bool qvalid = false;
             if (row < B) qvalid = (__ldg(p.slot_mask + (size_t)u * G::MW + (row >> 5)) >> (row & 31)) & 1u;
             const float inv = (qvalid && l > 0.f) ? 1.f / l : 0.f;
@@ -463,8 +529,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 store = store && qvalid;
                 orow = p.out + (size_t)h * tp.o_hs + (((size_t)t * tp.H + hq) * tp.W + w) * tp.o_ts;
             }
+            orow += ch * (D / 2);
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
+            for (int c = 0; c < D / 64; ++c) {
                 uint32_t o[32];
                 tmem_ld32(tO + c * 32, o);
                 tmem_wait_ld();
@@ -478,7 +545,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
                 }
             }
-            if (p.lse != nullptr && row < B)
+            if (p.lse != nullptr && row < B && ch == 0)
                 p.lse[(size_t)u * B + row] = (qvalid && l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
         }
     }
