@@ -543,12 +543,10 @@ veda_status gemm(const int8_t *As, const int8_t *Bs, int M, int N, int K, int ba
     veda_status st;
     if ((st = make_slices_map(&ma, As, M, kpad(K), batch, BM)) != VEDA_OK) return st;
     if ((st = make_slices_map(&mb, Bs, N, kpad(K), batch, BN)) != VEDA_OK) return st;
-    static bool attr = false;
-    if (!attr) {
+    {  // set per launch: the attribute belongs to the current device's context
         const cudaError_t e =
             cudaFuncSetAttribute(oz_gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
         if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute(oz_gemm): %s", cudaGetErrorString(e));
-        attr = true;
     }
     GemmArgs a = a0;
     a.M = M;

@@ -151,6 +151,9 @@ veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k
     const int hc = chunk_heads(Hh, heads_per_chunk);
     SlotLayout L;
     if ((st = slot_layout(hc, N, sh, d, k, w, &L)) != VEDA_OK) return st;
+    // the scorer's arrays are checked before anything is enqueued
+    if (!w->w1q || !w->b1q || !w->w2q || !w->b2q || !w->w1k || !w->b1k || !w->w2k || !w->b2k)
+        return fail(VEDA_ERR_NULL, "sparse_attention_host: scorer weight pointer is NULL");
     if (workspace_bytes < kSlots * L.total)
         return fail(VEDA_ERR_WORKSPACE, "sparse_attention_host: workspace %zu < %zu", workspace_bytes,
                     kSlots * L.total);
@@ -175,73 +178,83 @@ veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k
     VEDA_CU(cudaStreamWaitEvent(side.h2d, ev_start, 0));
     VEDA_CU(cudaStreamWaitEvent(side.d2h, ev_start, 0));
 
-    const size_t tok = align256((size_t)hc * N * d * 2);
-    const size_t zb = align256((size_t)hc * sh.NT * 3 * d * 4);
-    const uint16_t *src[3] = {q_host, k_host, v_host};
-    for (int c = 0; c < n_chunks; ++c) {
-        const int h0 = c * hc;
-        const int hn = (h0 + hc <= Hh) ? hc : Hh - h0;
-        char *slot = static_cast<char *>(workspace) + (size_t)(c % kSlots) * L.total;
-        uint16_t *in[3];
-        for (int j = 0; j < 3; ++j) in[j] = reinterpret_cast<uint16_t *>(slot + L.in + j * tok);
-        uint16_t *out = reinterpret_cast<uint16_t *>(slot + L.out);
-        float *zq = reinterpret_cast<float *>(slot + L.z), *zk = reinterpret_cast<float *>(slot + L.z + zb);
-        int32_t *cnt = reinterpret_cast<int32_t *>(slot + L.cnt);
-        uint32_t *mask = reinterpret_cast<uint32_t *>(slot + L.mask);
-        float *scores = reinterpret_cast<float *>(slot + L.scores);
-        int32_t *idx = reinterpret_cast<int32_t *>(slot + L.idx);
-        void *ws = slot + L.ws;
-        // device strides of the chunk buffers (same layout kind as the host tensors)
-        const int64_t dhs = head_major ? N * d : d;
-        const int64_t dts = head_major ? d : (int64_t)hn * d;
+    auto enqueue = [&]() -> veda_status {
+        const size_t tok = align256((size_t)hc * N * d * 2);
+        const size_t zb = align256((size_t)hc * sh.NT * 3 * d * 4);
+        const uint16_t *src[3] = {q_host, k_host, v_host};
+        for (int c = 0; c < n_chunks; ++c) {
+            const int h0 = c * hc;
+            const int hn = (h0 + hc <= Hh) ? hc : Hh - h0;
+            char *slot = static_cast<char *>(workspace) + (size_t)(c % kSlots) * L.total;
+            uint16_t *in[3];
+            for (int j = 0; j < 3; ++j) in[j] = reinterpret_cast<uint16_t *>(slot + L.in + j * tok);
+            uint16_t *out = reinterpret_cast<uint16_t *>(slot + L.out);
+            float *zq = reinterpret_cast<float *>(slot + L.z), *zk = reinterpret_cast<float *>(slot + L.z + zb);
+            int32_t *cnt = reinterpret_cast<int32_t *>(slot + L.cnt);
+            uint32_t *mask = reinterpret_cast<uint32_t *>(slot + L.mask);
+            float *scores = reinterpret_cast<float *>(slot + L.scores);
+            int32_t *idx = reinterpret_cast<int32_t *>(slot + L.idx);
+            void *ws = slot + L.ws;
+            // device strides of the chunk buffers (same layout kind as the host tensors)
+            const int64_t dhs = head_major ? N * d : d;
+            const int64_t dts = head_major ? d : (int64_t)hn * d;
 
-        // 1. H2D of chunk c into slot c % 2 once the attention of chunk c-2 has read it
-        if (c >= kSlots) VEDA_CU(cudaStreamWaitEvent(side.h2d, ev_infree[c - kSlots], 0));
-        for (int j = 0; j < 3; ++j) {
+            // 1. H2D of chunk c into slot c % 2 once the attention of chunk c-2 has read it
+            if (c >= kSlots) VEDA_CU(cudaStreamWaitEvent(side.h2d, ev_infree[c - kSlots], 0));
+            for (int j = 0; j < 3; ++j) {
+                if (head_major)
+                    VEDA_CU(cudaMemcpyAsync(in[j], src[j] + (size_t)h0 * N * d, (size_t)hn * N * d * 2,
+                                            cudaMemcpyHostToDevice, side.h2d));
+                else
+                    VEDA_CU(cudaMemcpy2DAsync(in[j], (size_t)hn * d * 2, src[j] + (size_t)h0 * d, (size_t)Hh * d * 2,
+                                              (size_t)hn * d * 2, (size_t)N, cudaMemcpyHostToDevice, side.h2d));
+            }
+            VEDA_CU(cudaEventRecord(ev_h2d[c], side.h2d));
+
+            // 2. the path on the caller's stream (token layout in and out)
+            VEDA_CU(cudaStreamWaitEvent(cs, ev_h2d[c], 0));
+            HeadCfgs hcf;
+            for (int h = 0; h < hn; ++h) { hcf.pt[h] = all.pt[h0 + h]; hcf.ph[h] = all.ph[h0 + h]; hcf.pw[h] = all.pw[h0 + h]; }
+            if ((st = launch_tile_pool_tokens(in[0], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
+                                              sh.NT, d, zq, cnt, mask, cs)) != VEDA_OK ||
+                (st = launch_tile_pool_tokens(in[1], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
+                                              sh.NT, d, zk, nullptr, nullptr, cs)) != VEDA_OK)
+                return st;
+            veda_scorer wc = *w;
+            const size_t o1 = (size_t)h0 * w->d_in * w->d_hidden, o2 = (size_t)h0 * w->d_hidden * w->d_lat;
+            wc.w1q += o1; wc.w1k += o1; wc.b1q += (size_t)h0 * w->d_hidden; wc.b1k += (size_t)h0 * w->d_hidden;
+            wc.w2q += o2; wc.w2k += o2; wc.b2q += (size_t)h0 * w->d_lat; wc.b2k += (size_t)h0 * w->d_lat;
+            if ((st = veda_tile_score_pooled(zq, zk, cnt, hn, sh.NT, d, &wc, scores, ws, L.ws_bytes, cs)) != VEDA_OK)
+                return st;
+            if ((st = veda_select_topk(scores, hn, sh.NT, k, idx, cs)) != VEDA_OK) return st;
+            if (c >= kSlots) VEDA_CU(cudaStreamWaitEvent(cs, ev_d2h[c - kSlots], 0));  // out slot drained
+            const float scale = 1.0f / std::sqrt((float)d);
+            if ((st = launch_sparse_attn_tok(in[0], in[1], in[2], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h,
+                                             lat.w, sh.B, sh.NT, d, idx, mask, k, scale, out, dhs, dts, nullptr, 0,
+                                             hn * sh.NT, cs)) !=
+                VEDA_OK)
+                return st;
+            VEDA_CU(cudaEventRecord(ev_infree[c], cs));  // the attention was the last reader of Q/K/V
+            VEDA_CU(cudaEventRecord(ev_comp[c], cs));
+
+            // 3. D2H of chunk c
+            VEDA_CU(cudaStreamWaitEvent(side.d2h, ev_comp[c], 0));
             if (head_major)
-                VEDA_CU(cudaMemcpyAsync(in[j], src[j] + (size_t)h0 * N * d, (size_t)hn * N * d * 2,
-                                        cudaMemcpyHostToDevice, side.h2d));
+                VEDA_CU(cudaMemcpyAsync(o_host + (size_t)h0 * N * d, out, (size_t)hn * N * d * 2, cudaMemcpyDeviceToHost,
+                                        side.d2h));
             else
-                VEDA_CU(cudaMemcpy2DAsync(in[j], (size_t)hn * d * 2, src[j] + (size_t)h0 * d, (size_t)Hh * d * 2,
-                                          (size_t)hn * d * 2, (size_t)N, cudaMemcpyHostToDevice, side.h2d));
+                VEDA_CU(cudaMemcpy2DAsync(o_host + (size_t)h0 * d, (size_t)Hh * d * 2, out, (size_t)hn * d * 2,
+                                          (size_t)hn * d * 2, (size_t)N, cudaMemcpyDeviceToHost, side.d2h));
+            VEDA_CU(cudaEventRecord(ev_d2h[c], side.d2h));
         }
-        VEDA_CU(cudaEventRecord(ev_h2d[c], side.h2d));
-
-        // 2. the path on the caller's stream (token layout in and out)
-        VEDA_CU(cudaStreamWaitEvent(cs, ev_h2d[c], 0));
-        HeadCfgs hcf;
-        for (int h = 0; h < hn; ++h) { hcf.pt[h] = all.pt[h0 + h]; hcf.ph[h] = all.ph[h0 + h]; hcf.pw[h] = all.pw[h0 + h]; }
-        if ((st = launch_tile_pool_tokens(in[0], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
-                                          sh.NT, d, zq, cnt, mask, cs)) != VEDA_OK ||
-            (st = launch_tile_pool_tokens(in[1], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
-                                          sh.NT, d, zk, nullptr, nullptr, cs)) != VEDA_OK)
-            return st;
-        veda_scorer wc = *w;
-        const size_t o1 = (size_t)h0 * w->d_in * w->d_hidden, o2 = (size_t)h0 * w->d_hidden * w->d_lat;
-        wc.w1q += o1; wc.w1k += o1; wc.b1q += (size_t)h0 * w->d_hidden; wc.b1k += (size_t)h0 * w->d_hidden;
-        wc.w2q += o2; wc.w2k += o2; wc.b2q += (size_t)h0 * w->d_lat; wc.b2k += (size_t)h0 * w->d_lat;
-        if ((st = veda_tile_score_pooled(zq, zk, cnt, hn, sh.NT, d, &wc, scores, ws, L.ws_bytes, cs)) != VEDA_OK)
-            return st;
-        if ((st = veda_select_topk(scores, hn, sh.NT, k, idx, cs)) != VEDA_OK) return st;
-        if (c >= kSlots) VEDA_CU(cudaStreamWaitEvent(cs, ev_d2h[c - kSlots], 0));  // out slot drained
-        const float scale = 1.0f / std::sqrt((float)d);
-        if ((st = launch_sparse_attn_tok(in[0], in[1], in[2], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h,
-                                         lat.w, sh.B, sh.NT, d, idx, mask, k, scale, out, dhs, dts, nullptr, 0,
-                                         hn * sh.NT, cs)) !=
-            VEDA_OK)
-            return st;
-        VEDA_CU(cudaEventRecord(ev_infree[c], cs));  // the attention was the last reader of Q/K/V
-        VEDA_CU(cudaEventRecord(ev_comp[c], cs));
-
-        // 3. D2H of chunk c
-        VEDA_CU(cudaStreamWaitEvent(side.d2h, ev_comp[c], 0));
-        if (head_major)
-            VEDA_CU(cudaMemcpyAsync(o_host + (size_t)h0 * N * d, out, (size_t)hn * N * d * 2, cudaMemcpyDeviceToHost,
-                                    side.d2h));
-        else
-            VEDA_CU(cudaMemcpy2DAsync(o_host + (size_t)h0 * d, (size_t)Hh * d * 2, out, (size_t)hn * d * 2,
-                                      (size_t)hn * d * 2, (size_t)N, cudaMemcpyDeviceToHost, side.d2h));
-        VEDA_CU(cudaEventRecord(ev_d2h[c], side.d2h));
+        return VEDA_OK;
+    };
+    if ((st = enqueue()) != VEDA_OK) {
+        // a mid-loop failure may leave H2D/D2H copies of the caller's host buffers queued on
+        // the side streams: let them finish before the caller can free or reuse the buffers
+        cudaStreamSynchronize(side.h2d);
+        cudaStreamSynchronize(side.d2h);
+        return st;
     }
     // the caller's stream completes only after the last D2H (the d2h stream is in order)
     VEDA_CU(cudaStreamWaitEvent(cs, ev_d2h[n_chunks - 1], 0));

@@ -262,12 +262,10 @@ static veda_status launch(const uint16_t *q, const uint16_t *k, const uint32_t *
     veda_status st;
     if ((st = make_tmap_bf16(&mq, q, rows, D, B)) != VEDA_OK) return st;
     if ((st = make_tmap_bf16(&mk, k, rows, D, B)) != VEDA_OK) return st;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
+    {  // set per launch: the attribute belongs to the current device's context
         cudaError_t e = cudaFuncSetAttribute(target_scores_kernel<B, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              G::SMEM);
         if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-        attr_set = true;
     }
     Params p;
     p.slot_mask = mask;
@@ -355,12 +353,10 @@ veda_status launch_recall(const int32_t *sp, const int32_t *fu, const int32_t *c
 {
     const size_t smem = (size_t)tgt::RC_WARPS * ((NT + 31) / 32) * sizeof(uint32_t);
     if (smem > 200 * 1024) return fail(VEDA_ERR_SHAPE, "tile_recall: n_tiles=%d too large", NT);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
+    if (smem > 48 * 1024) {  // set per launch: the attribute belongs to the current device's context
         cudaError_t e =
             cudaFuncSetAttribute(tgt::recall_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-        attr = smem;
     }
     tgt::recall_kernel<<<1, tgt::RC_THREADS, smem, s>>>(sp, fu, cnt, rows, NT, k, recall);
     count_launch();
