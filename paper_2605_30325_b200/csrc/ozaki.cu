@@ -76,6 +76,21 @@ __device__ __forceinline__ void digits4(const double (&x)[4], int e, uint32_t (&
     }
 }
 
+// Digit images: the split kernels write each operand pre-tiled in exactly the shared-memory
+// image one GEMM ring stage holds -- per (batch, block of BR rows, 64-byte K slab): NS
+// slices x BR rows x 64 bytes, 16-byte chunks SWIZZLE_64B-permuted (chunk c of row rr at
+// c ^ ((rr >> 1) & 3)) -- so the producer moves a stage with one contiguous bulk copy per
+// operand instead of NS x BR 64-byte TMA rows.  Rows R .. ceil(R/BR)*BR - 1 are written 0.
+struct Img {
+    int BR, nblk, nslab;  // rows per block, blocks per batch, 64-byte slabs per row
+    __device__ __forceinline__ int64_t word(int b, int r, int k, int s) const  // byte offset of the word at k (k % 4 == 0)
+    {
+        const int blk = r / BR, rr = r - blk * BR, slab = k >> 6, kb = k & 63;
+        const int c = (kb >> 4) ^ ((rr >> 1) & 3);
+        return ((((int64_t)(b * nblk + blk) * nslab + slab) * NS + s) * BR + rr) * 64 + (c << 4) + (kb & 15);
+    }
+};
+
 // GELU(x) = x Phi(x) (erf form, reading R8) in fp64 without the libdevice erf (which costs
 // ~70 FP64 instructions and made the layer-2 split FP64-bound): Phi on [-8, 8] from a
 // table of degree-5 Taylor polynomials around the centres of 768 intervals of width 1/48
@@ -120,7 +135,7 @@ __device__ __forceinline__ double gelu_tab_g(double x)
 template <typename T, int J, bool GELU, int WPR>
 __global__ void __launch_bounds__(256, GELU ? 4 : 1) split_rows_kernel(const T *__restrict__ X, int R, int K, int64_t sr,
                                                          int64_t sb, int Kp, int batch, int8_t *__restrict__ out,
-                                                         int32_t *__restrict__ ex)
+                                                         int32_t *__restrict__ ex, const Img img)
 {
     // WPR warps share a row (each holds J/WPR of its 128-column chunks, fewer registers ->
     // more resident warps); the row maximum is combined through shared memory.
@@ -136,14 +151,15 @@ __global__ void __launch_bounds__(256, GELU ? 4 : 1) split_rows_kernel(const T *
         __syncthreads();
     }
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, part = wi % WPR;
-    const int nbx = (R + RPB - 1) / RPB;
+    const int Rp = img.nblk * img.BR;  // rows of the image (R real + zero padding)
+    const int nbx = (Rp + RPB - 1) / RPB;
     // without GELU: one row group per block (grid nbx x batch), the loop runs once
     const int nblk = GELU ? nbx * batch : 1;
     int it = 0;
     for (int blk = GELU ? (int)blockIdx.x : 0; blk < nblk; blk += GELU ? (int)gridDim.x : 1, ++it) {
         const int b = GELU ? blk / nbx : (int)blockIdx.y;
         const int r = (GELU ? blk - b * nbx : (int)blockIdx.x) * RPB + wi / WPR;
-        const bool ok = r < R;
+        const bool ok = r < R, inimg = r < Rp;
         const T *x = X + b * sb + (int64_t)(ok ? r : 0) * sr;
         double v[JW][4];
         double m = 0.0;
@@ -169,10 +185,9 @@ __global__ void __launch_bounds__(256, GELU ? 4 : 1) split_rows_kernel(const T *
 #pragma unroll
             for (int p2 = 0; p2 < WPR; ++p2) m = fmax(m, s_max[it & 1][(wi / WPR) * WPR + p2]);
         }
-        if (!ok) continue;
-        const int e = row_exponent(m);
-        if (lane == 0 && part == 0) ex[(int64_t)b * R + r] = e;
-        int8_t *o = out + ((int64_t)b * NS * R + r) * Kp;
+        if (!inimg) continue;
+        const int e = row_exponent(m);  // padding rows: all values 0 -> all digits 0
+        if (ok && lane == 0 && part == 0) ex[(int64_t)b * R + r] = e;
 #pragma unroll
         for (int jj = 0; jj < JW; ++jj) {
             const int k = 128 * (part + WPR * jj) + 4 * lane;
@@ -180,7 +195,7 @@ __global__ void __launch_bounds__(256, GELU ? 4 : 1) split_rows_kernel(const T *
             uint32_t w[NS];
             digits4(v[jj], e, w);
 #pragma unroll
-            for (int s = 0; s < NS; ++s) *reinterpret_cast<uint32_t *>(o + (int64_t)s * R * Kp + k) = w[s];
+            for (int s = 0; s < NS; ++s) *reinterpret_cast<uint32_t *>(out + img.word(b, r, k, s)) = w[s];
         }
     }
 }
@@ -193,7 +208,7 @@ __global__ void __launch_bounds__(256, GELU ? 4 : 1) split_rows_kernel(const T *
 template <typename T>
 __global__ void __launch_bounds__(256) split_cols_kernel(const T *__restrict__ X, int R, int K, int64_t sk,
                                                          int64_t sb, int Kp, int8_t *__restrict__ out,
-                                                         int32_t *__restrict__ ex)
+                                                         int32_t *__restrict__ ex, const Img img)
 {
     __shared__ double s_m[8][32];
     __shared__ uint32_t s_d[NS][32][33];  // [slice][row][k word], padded
@@ -224,12 +239,11 @@ __global__ void __launch_bounds__(256) split_cols_kernel(const T *__restrict__ X
             for (int s = 0; s < NS; ++s) s_d[s][tx][wk] = w[s];
         }
         __syncthreads();
-        // write: slice s, row rr, word ww (32 words = 128 bytes per row chunk)
+        // write: slice s, row rr, word ww (rows past R: zero digits, already in s_d)
         for (int i = threadIdx.x; i < NS * 32 * 32; i += 256) {
             const int ww = i & 31, rr = (i >> 5) & 31, s = i >> 10;
-            if (r0 + rr < R && kc + 4 * ww < Kp)
-                *reinterpret_cast<uint32_t *>(out + ((int64_t)(b * NS + s) * R + r0 + rr) * Kp + kc + 4 * ww) =
-                    s_d[s][rr][ww];
+            if (r0 + rr < img.nblk * img.BR && kc + 4 * ww < Kp)
+                *reinterpret_cast<uint32_t *>(out + img.word(b, r0 + rr, kc + 4 * ww, s)) = s_d[s][rr][ww];
         }
         __syncthreads();
     }
@@ -342,9 +356,8 @@ __device__ __forceinline__ void epi_tile(const GemmArgs &g, uint32_t tl, int b, 
 }
 
 template <int BN, int EPI>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                                  const __grid_constant__ CUtensorMap tmB,
-                                                                  const GemmArgs g)
+__global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const int8_t *__restrict__ As,
+                                                                  const int8_t *__restrict__ Bs, const GemmArgs g)
 {
     using G = GemmGeo<BN>;
     extern __shared__ uint8_t smem_raw[];
@@ -369,8 +382,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
         mbar_init(OZ_DONE, 1);
         mbar_init(OZ_TFREE, 32 * EPI_WARPS);
         fence_barrier_init();
-        tma_prefetch_desc(&tmA);
-        tma_prefetch_desc(&tmB);
     }
     if (warp == 1) {
         tmem_alloc(smem_u32(tmem_slot), 512);
@@ -388,18 +399,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
     };
 
     if (warp == 0) {
-        if (lane == 0) {  // TMA producer: all NS slices of A and of B for one 64-byte K slab
+        if (lane == 0) {  // producer: the pre-tiled images of A and B for one 64-byte K slab
             int it = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 int b, m0, n0;
                 tile_coords(t, b, m0, n0);
+                const int8_t *a = As + ((int64_t)(b * nmb + m0 / BM) * g.nk) * G::A_BYTES;
+                const int8_t *bb = Bs + ((int64_t)(b * nnb + n0 / BN) * g.nk) * G::B_BYTES;
                 for (int kc = 0; kc < g.nk; ++kc, ++it) {
                     const int st = it % NSTAGE;
                     mbar_wait(OZ_EMPTY(st), ((uint32_t)(it / NSTAGE) & 1u) ^ 1u);
                     mbar_expect_tx(OZ_FULL(st), G::STAGE);
                     const uint32_t sa = sbase + st * G::STAGE;
-                    tma_load_4d(sa, &tmA, kc * BKB, m0, 0, b, OZ_FULL(st));
-                    tma_load_4d(sa + G::A_BYTES, &tmB, kc * BKB, n0, 0, b, OZ_FULL(st));
+                    bulk_load(sa, a + (int64_t)kc * G::A_BYTES, G::A_BYTES, OZ_FULL(st));
+                    bulk_load(sa + G::A_BYTES, bb + (int64_t)kc * G::B_BYTES, G::B_BYTES, OZ_FULL(st));
                 }
             }
         }
@@ -488,18 +501,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const __grid_c
 }
 
 // ---------------------------------------------------------------- host side
-veda_status make_slices_map(CUtensorMap *map, const int8_t *base, int rows, int Kp, int batch, int box_rows);
 
 int kpad(int K) { return (K + BKB - 1) / BKB * BKB; }
 
+inline Img image_of(int R, int K, int BR) { return Img{BR, (R + BR - 1) / BR, kpad(K) / BKB}; }
+
 template <typename T, bool GELU = false>
 veda_status split_rows(const T *X, int R, int K, int64_t sr, int64_t sb, int batch, int8_t *out, int32_t *ex,
-                       cudaStream_t s)
+                       int BR, cudaStream_t s)
 {
     const int Kp = kpad(K);
+    const Img img = image_of(R, K, BR);
+    const int Rp = img.nblk * BR;
     // one block per row group, or (GELU) as many as are resident, each looping over groups
     auto go = [&](auto kern, int rpb) {
-        const int nbx = (R + rpb - 1) / rpb, total = nbx * batch;
+        const int nbx = (Rp + rpb - 1) / rpb, total = nbx * batch;
         dim3 grid(nbx, batch);
         if (GELU) {
             static int per_sm = 0;  // per instantiation of split_rows<T, GELU>
@@ -508,7 +524,7 @@ veda_status split_rows(const T *X, int R, int K, int64_t sr, int64_t sb, int bat
             if (per_sm < 1) per_sm = 1;
             grid = dim3(std::min(total, per_sm * num_sms()), 1);
         }
-        kern<<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, batch, out, ex);
+        kern<<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, batch, out, ex, img);
     };
     if (Kp <= 128)
         go(split_rows_kernel<T, 1, GELU, 1>, 8);
@@ -526,10 +542,11 @@ veda_status split_rows(const T *X, int R, int K, int64_t sr, int64_t sb, int bat
 
 template <typename T>
 veda_status split_cols(const T *X, int R, int K, int64_t sk, int64_t sb, int batch, int8_t *out, int32_t *ex,
-                       cudaStream_t s)
+                       int BR, cudaStream_t s)
 {
-    dim3 grid((R + 31) / 32, batch);
-    split_cols_kernel<T><<<grid, 256, 0, s>>>(X, R, K, sk, sb, kpad(K), out, ex);
+    const Img img = image_of(R, K, BR);
+    dim3 grid((img.nblk * BR + 31) / 32, batch);
+    split_cols_kernel<T><<<grid, 256, 0, s>>>(X, R, K, sk, sb, kpad(K), out, ex, img);
     count_launch();
     return check_launch("ozaki split_cols");
 }
@@ -539,10 +556,8 @@ veda_status gemm(const int8_t *As, const int8_t *Bs, int M, int N, int K, int ba
                  cudaStream_t s)
 {
     using G = GemmGeo<BN>;
-    CUtensorMap ma, mb;
-    veda_status st;
-    if ((st = make_slices_map(&ma, As, M, kpad(K), batch, BM)) != VEDA_OK) return st;
-    if ((st = make_slices_map(&mb, Bs, N, kpad(K), batch, BN)) != VEDA_OK) return st;
+    if ((reinterpret_cast<uintptr_t>(As) | reinterpret_cast<uintptr_t>(Bs)) & 15u)
+        return fail(VEDA_ERR_ALIGN, "ozaki gemm: digit images must be 16-byte aligned");
     {  // set per launch: the attribute belongs to the current device's context
         const cudaError_t e =
             cudaFuncSetAttribute(oz_gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
@@ -555,34 +570,12 @@ veda_status gemm(const int8_t *As, const int8_t *Bs, int M, int N, int K, int ba
     a.batch = batch;
     const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    oz_gemm_kernel<BN, EPI><<<grid, GEMM_THREADS, G::SMEM, s>>>(ma, mb, a);
+    oz_gemm_kernel<BN, EPI><<<grid, GEMM_THREADS, G::SMEM, s>>>(As, Bs, a);
     count_launch();
     return check_launch("ozaki gemm");
 }
 
 }  // namespace oz
-
-veda_status oz::make_slices_map(CUtensorMap *map, const int8_t *base, int rows, int Kp, int batch, int box_rows)
-{
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return fail(VEDA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    cuuint64_t dims[4] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)NS, (cuuint64_t)batch};
-    cuuint64_t strides[3] = {(cuuint64_t)Kp, (cuuint64_t)Kp * rows, (cuuint64_t)Kp * rows * NS};
-    cuuint32_t box[4] = {(cuuint32_t)BKB, (cuuint32_t)box_rows, (cuuint32_t)NS, 1};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t *>(base), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(VEDA_ERR_CUDA, "cuTensorMapEncodeTiled (int8 slices) failed (%d)", (int)r);
-    return VEDA_OK;
-}
 
 // Taylor table of Phi for gelu_tab, uploaded once per device (static module memory)
 static veda_status phi_table_ready(cudaStream_t s)
@@ -618,11 +611,21 @@ static veda_status phi_table_ready(cudaStream_t s)
     return VEDA_OK;
 }
 
+// rows rounded up to whole image blocks: A operands in blocks of BM, B operands of the GEMM's BN
+static size_t rup(size_t r, size_t b) { return (r + b - 1) / b * b; }
+static size_t img_a_bytes(int NT, int din, int dh, int dl)
+{
+    return rup(NT, oz::BM) * std::max(oz::kpad(din), std::max(oz::kpad(dh), oz::kpad(dl)));
+}
+static size_t img_b_bytes(int NT, int din, int dh, int dl)
+{
+    return std::max(rup(dh, 96) * oz::kpad(din), std::max(rup(dl, 64) * oz::kpad(dh), rup(NT, 96) * oz::kpad(dl)));
+}
+
 size_t ozaki_workspace(int Hh, int NT, int din, int dh, int dl)
 {
-    const size_t k1 = oz::kpad(din), k2 = oz::kpad(dh), k3 = oz::kpad(dl);
-    size_t amax = std::max(k1, std::max(k2, k3)) * NT;
-    size_t bmax = std::max(dh * k1, std::max(dl * k2, NT * k3));
+    size_t amax = img_a_bytes(NT, din, dh, dl);
+    size_t bmax = img_b_bytes(NT, din, dh, dl);
     size_t emax = std::max((size_t)NT, std::max((size_t)dh, (size_t)dl));
     return align256((size_t)Hh * oz::NS * amax) + align256((size_t)Hh * oz::NS * bmax) +
            align256((size_t)Hh * NT * 4) + align256((size_t)Hh * emax * 4);
@@ -634,9 +637,8 @@ veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *
                                int dl, const float *const w_q[4], const float *const w_k[4], double *hidden,
                                double *eq, double *ek, float *scores, void *scratch, cudaStream_t s)
 {
-    const size_t k1 = oz::kpad(din), k2 = oz::kpad(dh), k3 = oz::kpad(dl);
-    const size_t amax = std::max(k1, std::max(k2, k3)) * NT;
-    const size_t bmax = std::max(dh * k1, std::max(dl * k2, NT * k3));
+    const size_t amax = img_a_bytes(NT, din, dh, dl);
+    const size_t bmax = img_b_bytes(NT, din, dh, dl);
     char *p = static_cast<char *>(scratch);
     int8_t *As = reinterpret_cast<int8_t *>(p); p += align256((size_t)Hh * oz::NS * amax);
     int8_t *Bs = reinterpret_cast<int8_t *>(p); p += align256((size_t)Hh * oz::NS * bmax);
@@ -649,26 +651,26 @@ veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *
         const float *const *w = side ? w_k : w_q;
         double *e = side ? ek : eq;
         // layer 1: pre-activation z W1 + b1
-        if ((st = oz::split_rows<float>(z, NT, din, din, (int64_t)NT * din, Hh, As, ea, s)) != VEDA_OK) return st;
-        if ((st = oz::split_cols<float>(w[0], dh, din, dh, (int64_t)din * dh, Hh, Bs, eb, s)) != VEDA_OK) return st;
+        if ((st = oz::split_rows<float>(z, NT, din, din, (int64_t)NT * din, Hh, As, ea, oz::BM, s)) != VEDA_OK) return st;
+        if ((st = oz::split_cols<float>(w[0], dh, din, dh, (int64_t)din * dh, Hh, Bs, eb, 96, s)) != VEDA_OK) return st;
         oz::GemmArgs a{};
         a.ea = ea; a.eb = eb; a.bias = w[1]; a.C = hidden;  // pre-activation z W1 + b1
 #ifdef VEDA_GELU_IN_GEMM  // measured slower inside the full path (2.7 vs 2.0 ms at Waver)
         if ((st = oz::gemm<96, oz::EPI_GELU>(As, Bs, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
-        if ((st = oz::split_rows<double>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, s)) != VEDA_OK) return st;
+        if ((st = oz::split_rows<double>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, oz::BM, s)) != VEDA_OK) return st;
 #else
         if ((st = oz::gemm<96, oz::EPI_BIAS>(As, Bs, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
         // layer 2: e = GELU(pre) W2 + b2 (the GELU is applied while splitting the rows)
-        if ((st = oz::split_rows<double, true>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, s)) != VEDA_OK)
+        if ((st = oz::split_rows<double, true>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, oz::BM, s)) != VEDA_OK)
             return st;
 #endif
-        if ((st = oz::split_cols<float>(w[2], dl, dh, dl, (int64_t)dh * dl, Hh, Bs, eb, s)) != VEDA_OK) return st;
+        if ((st = oz::split_cols<float>(w[2], dl, dh, dl, (int64_t)dh * dl, Hh, Bs, eb, 64, s)) != VEDA_OK) return st;
         a.bias = w[3]; a.C = e;
         if ((st = oz::gemm<64, oz::EPI_BIAS>(As, Bs, NT, dl, dh, Hh, a, s)) != VEDA_OK) return st;
     }
     // S_pred = e_q e_k^T / sqrt(d'), -inf on empty key tiles
-    if ((st = oz::split_rows<double>(eq, NT, dl, dl, (int64_t)NT * dl, Hh, As, ea, s)) != VEDA_OK) return st;
-    if ((st = oz::split_rows<double>(ek, NT, dl, dl, (int64_t)NT * dl, Hh, Bs, eb, s)) != VEDA_OK) return st;
+    if ((st = oz::split_rows<double>(eq, NT, dl, dl, (int64_t)NT * dl, Hh, As, ea, oz::BM, s)) != VEDA_OK) return st;
+    if ((st = oz::split_rows<double>(ek, NT, dl, dl, (int64_t)NT * dl, Hh, Bs, eb, 96, s)) != VEDA_OK) return st;
     oz::GemmArgs a{};
     a.ea = ea; a.eb = eb; a.cnt = cnt; a.C = scores; a.den = std::sqrt((double)dl);
     return oz::gemm<96, oz::EPI_SCORE>(As, Bs, NT, NT, dl, Hh, a, s);

@@ -185,6 +185,13 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const void *tmap, int3
         : "memory");
 }
 // 4-D tiled load (coordinates innermost first)
+// plain (non-tensor) bulk copy global -> shared, completing on an mbarrier; bytes % 16 == 0
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const void *tmap, int32_t c0, int32_t c1, int32_t c2,
                                             int32_t c3, uint32_t bar)
 {
