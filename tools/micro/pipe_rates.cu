@@ -25,6 +25,8 @@ __device__ __forceinline__ void fadd2(float &a, float &b, float c, float d)
 }
 __device__ __forceinline__ float ffma(float a, float b, float c) { float d; asm volatile("fma.rn.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c)); return d; }
 
+__device__ __forceinline__ uint32_t ex2h2(uint32_t x) { uint32_t y; asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
+__device__ __forceinline__ uint32_t ex2b2(uint32_t x) { uint32_t y; asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
 // MODE: 0 ex2, 1 ffma2, 2 fadd2, 3 fmnmx3, 4 fmnmx, 5 f2fp, 6 ffma, 7 ex2+fmnmx3 (1:1),
 // 8 ex2+f2fp (2:1), 9 ex2+ffma2 (2:1), 10 full softmax mix per pair (ffma2, 2 ex2, fadd2, f2fp),
 // 11 mode 10 + 2 fmnmx3 per pair
@@ -42,6 +44,8 @@ __global__ void kern(float *out, long long *cyc, float seed)
         for (int j = 0; j < 8; ++j) {
             float &a = v[2 * j], &b = v[2 * j + 1];
             if (MODE == 0) { a = ex2f(a); }
+            if (MODE == 12) { a = __uint_as_float(ex2h2(__float_as_uint(a))); }
+            if (MODE == 13) { a = __uint_as_float(ex2b2(__float_as_uint(a))); }
             if (MODE == 1) { ffma2(a, b, 0.999f, -0.001f); }
             if (MODE == 2) { fadd2(a, b, v[(2 * j + 2) & 15], v[(2 * j + 3) & 15]); }
             if (MODE == 3) { a = mx3(a, b, v[(2 * j + 5) & 15]); }
@@ -94,6 +98,8 @@ int main()
     cudaMalloc(&cyc, 148 * 64 * sizeof(long long));
     for (int W = 1; W <= 2; ++W) {
         run<0>("ex2 (MUFU)", 1, out, cyc, W);
+        run<12>("ex2.approx.f16x2 (per pair)", 1, out, cyc, W);
+        run<13>("ex2.approx.ftz.bf16x2 (per pair)", 1, out, cyc, W);
         run<1>("ffma2", 1, out, cyc, W);
         run<2>("fadd2", 1, out, cyc, W);
         run<3>("fmnmx3", 1, out, cyc, W);
