@@ -309,13 +309,14 @@ def run_ours(args):
     launches = veda.launch_count() - n0
     total_ms = start.elapsed_time(stop)
     ms_step_local = total_ms / args.steps
-    parts = {n: 0.0 for n in path.STEPS[path.mode]}
+    parts = {n: 0.0 for n in path.steps}
     for e in evs:
         for j, name in enumerate(parts):
             parts[name] += e[j].elapsed_time(e[j + 1]) / args.steps
     if path.mode == "tokens":  # the token-layout attention stores rows straight to token order
         parts["attn"] += parts.pop("untile")
-    per_step = sorted(e[0].elapsed_time(e[5]) for e in evs)  # each call, first to last step event
+    nst = len(path.steps)
+    per_step = sorted(e[0].elapsed_time(e[nst]) for e in evs)  # each call, first to last step event
 
     def pct(xs, f):
         return xs[min(len(xs) - 1, max(0, int(round(f * (len(xs) - 1)))))]
@@ -434,7 +435,6 @@ def run_ours(args):
     # HBM-bound steps: algorithmic bytes / time
     n_tok = pre.lat[0] * pre.lat[1] * pre.lat[2]
     pool_bytes = 2 * Hh * n_tok * d * 2 + 2 * Hh * NT * 3 * d * 4  # Q and K read once, Zq / Zk written
-    topk_bytes = Hh * NT * NT * 4 + Hh * NT * kk * 4                 # S read once, lists written
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(tp):
@@ -489,9 +489,14 @@ def run_ours(args):
                           "pool": {"bytes": pool_bytes, "ms": round(parts["pool"], 3),
                                    "gbs": round(pool_bytes / parts["pool"] / 1e6, 1),
                                    "frac": round(pool_bytes / parts["pool"] / 1e6 / peaks["hbm_gbs"], 3)},
-                          "topk": {"bytes": topk_bytes, "ms": round(parts["topk"], 3),
-                                   "gbs": round(topk_bytes / parts["topk"] / 1e6, 1),
-                                   "frac": round(topk_bytes / parts["topk"] / 1e6 / peaks["hbm_gbs"], 3)}},
+                          # phi + S_pred + top-k per 2-head chunk (veda_tile_select_pooled): the
+                          # [Hh, N_T, N_T] scores never exist; each chunk's 29.5 MB stays in L2
+                          "score_topk": {"ms": round(parts["score_topk"], 3),
+                                         "s_chunk_bytes": 2 * NT * NT * 4}} if "score_topk" in parts else
+                         {"peak_gbs": peaks["hbm_gbs"],
+                          "pool": {"bytes": pool_bytes, "ms": round(parts["pool"], 3),
+                                   "gbs": round(pool_bytes / parts["pool"] / 1e6, 1),
+                                   "frac": round(pool_bytes / parts["pool"] / 1e6 / peaks["hbm_gbs"], 3)}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

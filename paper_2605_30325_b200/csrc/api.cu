@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -349,6 +350,83 @@ veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32
     return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq, ek,
                               scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),
                               S(stream));
+}
+
+// Steps 2 (phi, S_pred) + 3 (top-k) without a [Hh][N_T][N_T] score tensor: phi_q / phi_k
+// for all heads, then per chunk of heads the pair scores into a [chunk][N_T][N_T] scratch
+// that the top-k reads back straight away (chunk <= 32 MB by default, so the scores stay
+// in the 126 MB L2 between the two kernels and never round-trip through HBM).
+static int select_chunk_heads(int Hh, int NT, int heads_per_chunk)
+{
+    if (heads_per_chunk > 0) return std::min(heads_per_chunk, Hh);
+    const size_t per_head = (size_t)NT * NT * sizeof(float);
+    const size_t budget = (size_t)32 << 20;
+    return (int)std::max<size_t>(1, std::min<size_t>((size_t)Hh, budget / per_head));
+}
+
+veda_status veda_tile_select_workspace(int32_t Hh, int32_t n_tiles, int32_t d, const veda_scorer *w,
+                                       int32_t heads_per_chunk, size_t *bytes)
+{
+    size_t b = 0;
+    veda_status st = veda_tile_score_workspace(Hh, n_tiles, d, w, &b);
+    if (st != VEDA_OK) return st;
+    if (heads_per_chunk < 0) return fail(VEDA_ERR_SHAPE, "tile_select_workspace: heads_per_chunk=%d < 0", heads_per_chunk);
+    const int hc = select_chunk_heads(Hh, n_tiles, heads_per_chunk);
+    *bytes = b + align256((size_t)hc * n_tiles * n_tiles * sizeof(float));
+    return VEDA_OK;
+}
+
+veda_status veda_tile_select_pooled(const float *zq, const float *zk, const int32_t *tile_count, int32_t Hh,
+                                    int32_t n_tiles, int32_t d, const veda_scorer *w, int32_t k,
+                                    int32_t heads_per_chunk, int32_t *idx, void *workspace, size_t workspace_bytes,
+                                    void *stream)
+{
+    if (!zq || !zk || !tile_count || !w || !idx || !workspace)
+        return fail(VEDA_ERR_NULL, "tile_select_pooled: NULL pointer");
+    if (!w->w1q || !w->b1q || !w->w2q || !w->b2q || !w->w1k || !w->b1k || !w->w2k || !w->b2k)
+        return fail(VEDA_ERR_NULL, "tile_select_pooled: NULL scorer weight");
+    size_t need = 0, score_ws = 0;
+    veda_status st = veda_tile_select_workspace(Hh, n_tiles, d, w, heads_per_chunk, &need);
+    if (st != VEDA_OK) return st;
+    if (k < 1 || k > n_tiles) return fail(VEDA_ERR_K_RANGE, "tile_select_pooled: k=%d outside [1, %d]", k, n_tiles);
+    if (workspace_bytes < need)
+        return fail(VEDA_ERR_WORKSPACE, "tile_select_pooled: workspace %zu < %zu", workspace_bytes, need);
+    if (!aligned16(workspace)) return fail(VEDA_ERR_ALIGN, "tile_select_pooled: workspace not aligned");
+    if ((st = check_arch()) != VEDA_OK) return st;
+    if (debug_mode() && (st = debug_validate(S(stream), [&](uint32_t *f) {
+                             veda_status e = launch_validate_finite_f32(zq, (int64_t)Hh * n_tiles * w->d_in, f, S(stream));
+                             if (e == VEDA_OK) e = launch_validate_finite_f32(zk, (int64_t)Hh * n_tiles * w->d_in, f, S(stream));
+                             return e;
+                         })) != VEDA_OK)
+        return st;
+    veda_tile_score_workspace(Hh, n_tiles, d, w, &score_ws);
+    const size_t rows = (size_t)Hh * n_tiles;
+    char *p = static_cast<char *>(workspace);
+    p += 2 * align256(rows * w->d_in * sizeof(float));  // Zq/Zk region unused here
+    double *hid = reinterpret_cast<double *>(p); p += align256(rows * w->d_hidden * sizeof(double));
+    double *eq = reinterpret_cast<double *>(p); p += align256(rows * w->d_lat * sizeof(double));
+    double *ek = reinterpret_cast<double *>(p); p += align256(rows * w->d_lat * sizeof(double));
+    void *oz_scratch = p;
+    float *s_chunk = reinterpret_cast<float *>(static_cast<char *>(workspace) + score_ws);
+    const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
+    if ((st = launch_ozaki_phi(zq, zk, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq, ek, oz_scratch,
+                               S(stream))) != VEDA_OK)
+        return st;
+    const int hc = select_chunk_heads(Hh, n_tiles, heads_per_chunk);
+    for (int h0 = 0; h0 < Hh; h0 += hc) {
+        const int hn = std::min(hc, Hh - h0);
+        const size_t e0 = (size_t)h0 * n_tiles * w->d_lat;
+        if ((st = launch_ozaki_pair_scores(eq + e0, ek + e0, tile_count + (size_t)h0 * n_tiles, hn, n_tiles, w->d_in,
+                                           w->d_hidden, w->d_lat, s_chunk, oz_scratch, S(stream))) != VEDA_OK)
+            return st;
+        if (debug_mode() && (st = debug_validate(S(stream), [&](uint32_t *f) {
+                                 return launch_validate_scores(s_chunk, (int64_t)hn * n_tiles * n_tiles, f, S(stream));
+                             })) != VEDA_OK)
+            return st;
+        if ((st = launch_topk(s_chunk, hn, n_tiles, k, idx + (size_t)h0 * n_tiles * k, S(stream))) != VEDA_OK)
+            return st;
+    }
+    return VEDA_OK;
 }
 
 veda_status veda_select_topk(const float *scores, int32_t Hh, int32_t n_tiles, int32_t k, int32_t *idx, void *stream)

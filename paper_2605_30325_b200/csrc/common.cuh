@@ -83,6 +83,11 @@ size_t ozaki_workspace(int Hh, int NT, int din, int dh, int dl);
 veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *cnt, int Hh, int NT, int din, int dh,
                                int dl, const float *const w_q[4], const float *const w_k[4], double *hidden,
                                double *eq, double *ek, float *scores, void *scratch, cudaStream_t s);
+veda_status launch_ozaki_phi(const float *zq, const float *zk, int Hh, int NT, int din, int dh, int dl,
+                             const float *const w_q[4], const float *const w_k[4], double *hidden, double *eq,
+                             double *ek, void *scratch, cudaStream_t s);
+veda_status launch_ozaki_pair_scores(const double *eq, const double *ek, const int32_t *cnt, int Hh, int NT, int din,
+                                     int dh, int dl, float *scores, void *scratch, cudaStream_t s);
 veda_status launch_target_scores(const uint16_t *q, const uint16_t *k, const uint32_t *mask, const float *lse,
                                  int Hh, int NT, int B, int d, float scale, float *out, cudaStream_t s);
 veda_status launch_permute_scalar(const float *x, int64_t hs, const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp,
@@ -102,6 +107,7 @@ veda_status launch_validate_index(const int32_t *idx, int64_t rows, int n_tiles,
 veda_status launch_validate_finite(const uint16_t *x, int64_t hs, int64_t ts, int Hh, int64_t n, int d,
                                    uint32_t *flags, cudaStream_t s);
 veda_status launch_validate_scores(const float *scores, int64_t n, uint32_t *flags, cudaStream_t s);
+veda_status launch_validate_finite_f32(const float *x, int64_t n, uint32_t *flags, cudaStream_t s);
 bool debug_mode();
 void set_debug_mode(bool on);
 veda_status debug_validate(cudaStream_t s, const std::function<veda_status(uint32_t *)> &enqueue);

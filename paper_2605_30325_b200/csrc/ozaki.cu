@@ -631,11 +631,11 @@ size_t ozaki_workspace(int Hh, int NT, int din, int dh, int dl)
            align256((size_t)Hh * NT * 4) + align256((size_t)Hh * emax * 4);
 }
 
-// phi_q, phi_k and S_pred from pooled descriptors on the INT8 tensor cores.
+// phi_q, phi_k (Eq. 6's MLPs) from pooled descriptors on the INT8 tensor cores.
 // hidden [Hh][NT][dh], eq / ek [Hh][NT][dl] are fp64 buffers; scratch >= ozaki_workspace.
-veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *cnt, int Hh, int NT, int din, int dh,
-                               int dl, const float *const w_q[4], const float *const w_k[4], double *hidden,
-                               double *eq, double *ek, float *scores, void *scratch, cudaStream_t s)
+veda_status launch_ozaki_phi(const float *zq, const float *zk, int Hh, int NT, int din, int dh, int dl,
+                             const float *const w_q[4], const float *const w_k[4], double *hidden, double *eq,
+                             double *ek, void *scratch, cudaStream_t s)
 {
     const size_t amax = img_a_bytes(NT, din, dh, dl);
     const size_t bmax = img_b_bytes(NT, din, dh, dl);
@@ -655,25 +655,45 @@ veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *
         if ((st = oz::split_cols<float>(w[0], dh, din, dh, (int64_t)din * dh, Hh, Bs, eb, 96, s)) != VEDA_OK) return st;
         oz::GemmArgs a{};
         a.ea = ea; a.eb = eb; a.bias = w[1]; a.C = hidden;  // pre-activation z W1 + b1
-#ifdef VEDA_GELU_IN_GEMM  // measured slower inside the full path (2.7 vs 2.0 ms at Waver)
-        if ((st = oz::gemm<96, oz::EPI_GELU>(As, Bs, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
-        if ((st = oz::split_rows<double>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, oz::BM, s)) != VEDA_OK) return st;
-#else
         if ((st = oz::gemm<96, oz::EPI_BIAS>(As, Bs, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
         // layer 2: e = GELU(pre) W2 + b2 (the GELU is applied while splitting the rows)
         if ((st = oz::split_rows<double, true>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, oz::BM, s)) != VEDA_OK)
             return st;
-#endif
         if ((st = oz::split_cols<float>(w[2], dl, dh, dl, (int64_t)dh * dl, Hh, Bs, eb, 64, s)) != VEDA_OK) return st;
         a.bias = w[3]; a.C = e;
         if ((st = oz::gemm<64, oz::EPI_BIAS>(As, Bs, NT, dl, dh, Hh, a, s)) != VEDA_OK) return st;
     }
-    // S_pred = e_q e_k^T / sqrt(d'), -inf on empty key tiles
+    return VEDA_OK;
+}
+
+// S_pred = e_q e_k^T / sqrt(d'), -inf on empty key tiles, for Hh heads (pointers at the
+// first head); scratch >= ozaki_workspace(Hh, ...).
+veda_status launch_ozaki_pair_scores(const double *eq, const double *ek, const int32_t *cnt, int Hh, int NT, int din,
+                                     int dh, int dl, float *scores, void *scratch, cudaStream_t s)
+{
+    const size_t amax = img_a_bytes(NT, din, dh, dl);
+    const size_t bmax = img_b_bytes(NT, din, dh, dl);
+    char *p = static_cast<char *>(scratch);
+    int8_t *As = reinterpret_cast<int8_t *>(p); p += align256((size_t)Hh * oz::NS * amax);
+    int8_t *Bs = reinterpret_cast<int8_t *>(p); p += align256((size_t)Hh * oz::NS * bmax);
+    int32_t *ea = reinterpret_cast<int32_t *>(p); p += align256((size_t)Hh * NT * 4);
+    int32_t *eb = reinterpret_cast<int32_t *>(p);
+    veda_status st;
     if ((st = oz::split_rows<double>(eq, NT, dl, dl, (int64_t)NT * dl, Hh, As, ea, oz::BM, s)) != VEDA_OK) return st;
     if ((st = oz::split_rows<double>(ek, NT, dl, dl, (int64_t)NT * dl, Hh, Bs, eb, 96, s)) != VEDA_OK) return st;
     oz::GemmArgs a{};
     a.ea = ea; a.eb = eb; a.cnt = cnt; a.C = scores; a.den = std::sqrt((double)dl);
     return oz::gemm<96, oz::EPI_SCORE>(As, Bs, NT, NT, dl, Hh, a, s);
+}
+
+// phi_q, phi_k and S_pred for all heads (the unfused form of veda_tile_score)
+veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *cnt, int Hh, int NT, int din, int dh,
+                               int dl, const float *const w_q[4], const float *const w_k[4], double *hidden,
+                               double *eq, double *ek, float *scores, void *scratch, cudaStream_t s)
+{
+    veda_status st = launch_ozaki_phi(zq, zk, Hh, NT, din, dh, dl, w_q, w_k, hidden, eq, ek, scratch, s);
+    if (st != VEDA_OK) return st;
+    return launch_ozaki_pair_scores(eq, ek, cnt, Hh, NT, din, dh, dl, scores, scratch, s);
 }
 
 }  // namespace veda

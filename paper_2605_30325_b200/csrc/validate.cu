@@ -65,6 +65,15 @@ __global__ void validate_scores_kernel(const float *__restrict__ s, int64_t n, u
     if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, VEDA_FLAG_NONFINITE);
 }
 
+// fp32 inputs (pooled descriptors): NaN or +-inf is flagged
+__global__ void validate_finite_f32_kernel(const float *__restrict__ x, int64_t n, uint32_t *__restrict__ flags)
+{
+    uint32_t bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= isfinite(__ldg(x + i)) ? 0u : 1u;
+    if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, VEDA_FLAG_NONFINITE);
+}
+
 std::atomic<int> g_debug{-1};
 
 // per-device flag word of debug mode (allocated on first use, debug mode only)
@@ -106,6 +115,14 @@ veda_status launch_validate_scores(const float *scores, int64_t n, uint32_t *fla
     validate_scores_kernel<<<4 * num_sms(), 256, 0, s>>>(scores, n, flags);
     count_launch();
     return check_launch("validate_scores");
+}
+
+veda_status launch_validate_finite_f32(const float *x, int64_t n, uint32_t *flags, cudaStream_t s)
+{
+    if (n == 0) return VEDA_OK;
+    validate_finite_f32_kernel<<<4 * num_sms(), 256, 0, s>>>(x, n, flags);
+    count_launch();
+    return check_launch("validate_finite_f32");
 }
 
 bool debug_mode()

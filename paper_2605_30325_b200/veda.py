@@ -32,7 +32,8 @@ EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_worksp
            "veda_sq_err", "veda_sparse_attention_host_workspace", "veda_sparse_attention_host",
            "veda_tile_pool", "veda_sparse_attn_fwd_tokens", "veda_sparse_attn_fwd_tokens_units",
            "veda_tile_pool_heads", "veda_validate_index", "veda_validate_finite", "veda_set_debug",
-           "veda_tile_pool_local", "veda_sparse_attn_fwd_tokens_local"]
+           "veda_tile_pool_local", "veda_sparse_attn_fwd_tokens_local", "veda_tile_select_workspace",
+           "veda_tile_select_pooled"]
 
 
 class VedaError(RuntimeError):
@@ -77,6 +78,8 @@ def load(path: str = LIB_PATH):
         "veda_tile_permute": ([P, i64, i64, Latent, P, i32, i32, P, P, P, P], i32),
         "veda_tile_permute_pool": ([P, i64, i64, Latent, P, i32, i32, P, P, P, P, P], i32),
         "veda_tile_score_pooled": ([P, P, P, i32, i32, i32, P, P, P, sz, P], i32),
+        "veda_tile_select_workspace": ([i32, i32, i32, P, i32, P], i32),
+        "veda_tile_select_pooled": ([P, P, P, i32, i32, i32, P, i32, i32, P, P, sz, P], i32),
         "veda_tile_score": ([P, P, P, P, i32, i32, i32, i32, P, P, P, sz, P], i32),
         "veda_select_topk": ([P, i32, i32, i32, P, P], i32),
         "veda_sparse_attn_fwd": ([P, P, P, P, P, i32, i32, i32, i32, i32, f32, P, P, P], i32),
@@ -374,6 +377,43 @@ def tile_score_pooled(zq, zk, tile_count, scorer: Scorer, workspace: ScoreWorksp
     return out
 
 
+def select_chunk_heads(Hh: int, n_tiles: int, heads_per_chunk: int = 0) -> int:
+    """Heads per score chunk of veda_tile_select_pooled (mirrors the library: as many heads
+    as fit 32 MB of fp32 scores, at least one, unless given)."""
+    if heads_per_chunk > 0:
+        return min(heads_per_chunk, Hh)
+    return max(1, min(Hh, (32 << 20) // (n_tiles * n_tiles * 4)))
+
+
+class SelectWorkspace:
+    """Caller-owned workspace for tile_select_pooled (score + top-k without a full S)."""
+
+    def __init__(self, Hh, n_tiles, d, scorer: Scorer, device, heads_per_chunk=0):
+        n = ctypes.c_size_t(0)
+        _check(load().veda_tile_select_workspace(Hh, n_tiles, d, ctypes.byref(scorer), heads_per_chunk,
+                                                 ctypes.byref(n)), "tile_select_workspace")
+        self.nbytes = n.value
+        self.heads_per_chunk = heads_per_chunk
+        self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+
+
+def tile_select_pooled(zq, zk, tile_count, scorer: Scorer, k: int, heads_per_chunk: int = 0,
+                       workspace: SelectWorkspace = None, out=None):
+    """Kept-tile lists [Hh, N_T, k] from pooled descriptors (phi, S_pred per head chunk, top-k)."""
+    _need_cuda(zq, zk, tile_count)
+    Hh, NT, din = zq.shape
+    d = din // 3
+    if workspace is None:
+        workspace = SelectWorkspace(Hh, NT, d, scorer, zq.device, heads_per_chunk)
+    if out is None:
+        out = torch.empty((Hh, NT, k), dtype=torch.int32, device=zq.device)
+    st = load().veda_tile_select_pooled(_ptr(zq), _ptr(zk), _ptr(tile_count), Hh, NT, d, ctypes.byref(scorer), k,
+                                        workspace.heads_per_chunk, _ptr(out), _ptr(workspace.buf), workspace.nbytes,
+                                        _stream())
+    _check(st, "tile_select_pooled")
+    return out
+
+
 def select_topk(scores: torch.Tensor, k: int, out=None):
     _need_cuda(scores)
     Hh, NT, _ = scores.shape
@@ -483,18 +523,21 @@ class SparseAttention:
     three).  Steps (Alg. 2 + Eq. 2):
 
     * ``mode="tokens"`` (default): tile_pool Q/K (TripPool read
-      straight from token order) -> tile_score_pooled -> select_topk ->
-      sparse_attn_fwd_tokens (tiles TMA'd from token order, rows stored to token order);
-      no tiled copy of Q, K, V or O exists;
+      straight from token order) -> tile_select_pooled (phi, S_pred and top-k per chunk of
+      heads: no [Hh, N_T, N_T] score tensor) -> sparse_attn_fwd_tokens (tiles TMA'd from
+      token order, rows stored to token order); no tiled copy of Q, K, V or O exists.
+      ``keep_scores=True`` runs tile_score_pooled -> select_topk instead and keeps S in
+      ``self.scores`` (parity tests; the lists are bit-identical);
     * ``mode="tiled"``: permute Q/K/V -> tile_score -> select_topk -> sparse_attn_fwd ->
       unpermute (the five-call form of include/veda.h; bit-identical output).
     """
 
-    STEPS = {"tokens": ("pool", "score", "topk", "attn", "untile"),
+    STEPS = {"tokens": ("pool", "score_topk", "attn", "untile"),
+             "tokens_keep": ("pool", "score", "topk", "attn", "untile"),
              "tiled": ("permute", "score", "topk", "attn", "unpermute")}
 
     def __init__(self, lat, cfgs, Hh, d, scorer_weights: dict, sparsity=None, k=None, device="cuda",
-                 mode="tokens", units=None, head_range=None):
+                 mode="tokens", units=None, head_range=None, keep_scores=False):
         """``units=(begin, end)`` (tokens mode): a rank's share under shard.unit_range of the
         flattened (head, query tile) units of this Hh-head call.  Pooling (on the call's
         padded grid, veda_tile_pool_heads), scoring and top-k then run for the heads the
@@ -508,8 +551,10 @@ class SparseAttention:
         head-aware tiling), but q, k, v, out and scorer_weights hold ONLY those heads
         ([h1 - h0, N, d]; the Ulysses front end's head shards).  Outputs are bit-identical
         to the same heads of the whole call."""
-        if mode not in self.STEPS:
-            raise VedaError(f"mode must be one of {list(self.STEPS)}")
+        if mode not in ("tokens", "tiled"):
+            raise VedaError("mode must be one of ['tokens', 'tiled']")
+        self.keep_scores = bool(keep_scores) or mode == "tiled"
+        self.steps = self.STEPS["tiled" if mode == "tiled" else ("tokens_keep" if self.keep_scores else "tokens")]
         if (units is not None or head_range is not None) and mode != "tokens":
             raise VedaError("units / head_range: tokens mode only")
         if units is not None and head_range is not None:
@@ -539,7 +584,7 @@ class SparseAttention:
             self.zk = torch.empty((Hb, NT, 3 * d), dtype=torch.float32, device=dev)
         self.cnt = torch.empty((Hb, NT), dtype=torch.int32, device=dev)
         self.mask = torch.empty((Hb, NT, B // 32), dtype=torch.int32, device=dev)
-        self.scores = torch.empty((Hb, NT, NT), dtype=torch.float32, device=dev)
+        self.scores = torch.empty((Hb, NT, NT), dtype=torch.float32, device=dev) if self.keep_scores else None
         self.idx = torch.empty((Hb, NT, self.k), dtype=torch.int32, device=dev)
         self.heads = range(Hh)
         if self.head_range is not None:
@@ -556,7 +601,10 @@ class SparseAttention:
             self.w_sub = {n: t[h0:h1] for n, t in scorer_weights.items()}
             if h1 > h0:
                 self.scorer = make_scorer(self.w_sub)
-        self.ws = ScoreWorkspace(max(1, len(self.heads)), NT, d, self.scorer, dev)
+        if self.keep_scores:
+            self.ws = ScoreWorkspace(max(1, len(self.heads)), NT, d, self.scorer, dev)
+        else:
+            self.ws = SelectWorkspace(max(1, len(self.heads)), NT, d, self.scorer, dev)
 
     def tiled(self, q, k, v):
         """Tiled copies (q~, k~, v~) of the inputs (for the oracle-mask / target tools)."""
@@ -576,11 +624,15 @@ class SparseAttention:
                               device=q.device)
         ev = events or [None] * 6
 
-        def mark(i):
-            if ev[i] is not None:
-                ev[i].record()
+        nmark = [0]
 
-        mark(0)
+        def mark():  # events[i] after the i-th step (self.steps), events[0] at the start
+            i = nmark[0]
+            if i < len(ev) and ev[i] is not None:
+                ev[i].record()
+            nmark[0] += 1
+
+        mark()
         if self.mode == "tokens":
             if not (k.stride() == q.stride() and v.stride() == q.stride()):
                 raise VedaError("q, k, v must share strides")
@@ -600,19 +652,28 @@ class SparseAttention:
                                                 _ptr(self.zq), _ptr(self.cnt), _ptr(self.mask), s), "tile_pool_heads(q)")
                 _check(lib.veda_tile_pool_heads(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, h0, h1,
                                                 _ptr(self.zk), None, None, s), "tile_pool_heads(k)")
-            mark(1)
+            mark()
             # score / top-k buffers: the whole call's rows (units) or the shard's own (head_range)
             R = (lambda t, a, b: t[a:b]) if self.head_range is None else (lambda t, a, b: t)
-            if h1 > h0:
-                _check(lib.veda_tile_score_pooled(_ptr(R(self.zq, h0, h1)), _ptr(R(self.zk, h0, h1)),
-                                                  _ptr(R(self.cnt, h0, h1)), h1 - h0, NT, d, ctypes.byref(self.scorer),
-                                                  _ptr(R(self.scores, h0, h1)), _ptr(self.ws.buf), self.ws.nbytes, s),
-                       "tile_score_pooled")
-            mark(2)
-            if h1 > h0:
-                _check(lib.veda_select_topk(_ptr(R(self.scores, h0, h1)), h1 - h0, NT, self.k,
-                                            _ptr(R(self.idx, h0, h1)), s), "select_topk")
-            mark(3)
+            if self.keep_scores:
+                if h1 > h0:
+                    _check(lib.veda_tile_score_pooled(_ptr(R(self.zq, h0, h1)), _ptr(R(self.zk, h0, h1)),
+                                                      _ptr(R(self.cnt, h0, h1)), h1 - h0, NT, d,
+                                                      ctypes.byref(self.scorer), _ptr(R(self.scores, h0, h1)),
+                                                      _ptr(self.ws.buf), self.ws.nbytes, s), "tile_score_pooled")
+                mark()
+                if h1 > h0:
+                    _check(lib.veda_select_topk(_ptr(R(self.scores, h0, h1)), h1 - h0, NT, self.k,
+                                                _ptr(R(self.idx, h0, h1)), s), "select_topk")
+                mark()
+            else:
+                if h1 > h0:
+                    _check(lib.veda_tile_select_pooled(_ptr(R(self.zq, h0, h1)), _ptr(R(self.zk, h0, h1)),
+                                                       _ptr(R(self.cnt, h0, h1)), h1 - h0, NT, d,
+                                                       ctypes.byref(self.scorer), self.k, self.ws.heads_per_chunk,
+                                                       _ptr(R(self.idx, h0, h1)), _ptr(self.ws.buf), self.ws.nbytes,
+                                                       s), "tile_select_pooled")
+                mark()
             if self.units is None:
                 _check(lib.veda_sparse_attn_fwd_tokens(_ptr(q), _ptr(k), _ptr(v), q.stride(0), q.stride(1), lat, cfg,
                                                        Hh, d, _ptr(self.idx), _ptr(self.mask), self.k, 0.0, _ptr(out),
@@ -628,8 +689,8 @@ class SparseAttention:
                                                              _ptr(out), out.stride(0), out.stride(1), None,
                                                              self.units[0], self.units[1], s),
                        "sparse_attn_fwd_tokens_units")
-            mark(4)
-            mark(5)
+            mark()  # attn
+            mark()  # untile (fused into the attention epilogue)
             return out
         # Q/K tiling and TripPool as two HBM-bound passes: measured faster than the fused
         # veda_tile_permute_pool (its extra registers halve the occupancy of the copy)
@@ -639,28 +700,32 @@ class SparseAttention:
                                      s), "tile_permute(k)")
         _check(lib.veda_tile_permute(_ptr(v), v.stride(0), v.stride(1), lat, cfg, Hh, d, _ptr(self.vt), None, None,
                                      s), "tile_permute(v)")
-        mark(1)
+        mark()
         _check(lib.veda_tile_score(_ptr(self.qt), _ptr(self.kt), _ptr(self.cnt), _ptr(self.mask), Hh, NT, B, d,
                                    ctypes.byref(self.scorer), _ptr(self.scores), _ptr(self.ws.buf), self.ws.nbytes, s),
                "tile_score")
-        mark(2)
+        mark()
         _check(lib.veda_select_topk(_ptr(self.scores), Hh, NT, self.k, _ptr(self.idx), s), "select_topk")
-        mark(3)
+        mark()
         _check(lib.veda_sparse_attn_fwd(_ptr(self.qt), _ptr(self.kt), _ptr(self.vt), _ptr(self.idx), _ptr(self.mask),
                                         Hh, NT, B, d, self.k, 0.0, _ptr(self.ot), None, s), "sparse_attn_fwd")
-        mark(4)
+        mark()
         _check(lib.veda_tile_unpermute(_ptr(self.ot), lat, cfg, Hh, d, _ptr(out), out.stride(0), out.stride(1), s),
                "tile_unpermute")
-        mark(5)
+        mark()
         return out
 
     @property
     def LAUNCHES_PER_CALL(self):
-        """Kernel launches of one call.  Scorer (INT8 Ozaki) = per side 2 x (split rows, split
-        cols, GEMM), then 2 splits + the score GEMM = 15.  tokens: pool x2, scorer, topk,
-        attn;  tiled: permute x3, pool x2, scorer, topk, attn, unpermute."""
-        n = 15
-        return {"tokens": 2 + n + 1 + 1, "tiled": 3 + 2 + n + 1 + 1 + 1}
+        """Kernel launches of one call.  Scorer (INT8 Ozaki): phi = per side 2 x (split rows,
+        split cols, GEMM) = 12; per chunk of heads 2 splits + the score GEMM (+ the top-k in
+        the fused select).  tokens: pool x2, phi, chunks x (splits, GEMM, top-k), attn (one
+        chunk with keep_scores); tiled: permute x3, pool x2, phi, 3, topk, attn, unpermute."""
+        phi = 12
+        nh = max(1, len(self.heads))
+        chunks = 1 if self.keep_scores else -(-nh // select_chunk_heads(nh, self.shape.n_tiles,
+                                                                         self.ws.heads_per_chunk))
+        return {"tokens": 2 + phi + 4 * chunks + 1, "tiled": 3 + 2 + phi + 3 + 1 + 1 + 1}
 
     def run_host(self, q, k, v, out=None, heads_per_chunk: int = 0):
         """The same call on HOST tensors (veda_sparse_attention_host): q, k, v, out are

@@ -312,7 +312,8 @@ def test_end_to_end_path_object(V, oracle, mode):
     s = V.tile_score(qt, kt, cnt, mask, V.make_scorer(w))
     idx = V.select_topk(s, path.k)
     o2 = V.tile_unpermute(V.sparse_attn_fwd(qt, kt, vt, idx, mask), c.lat, c.cfgs)
-    assert torch.equal(path.idx, idx) and torch.equal(path.scores, s) and torch.equal(o, o2)
+    assert torch.equal(path.idx, idx) and torch.equal(o, o2)
+    assert path.scores is None if mode == "tokens" else torch.equal(path.scores, s)
     # deterministic: a second call is bit-identical
     assert torch.equal(path(q, k, v), o)
 
@@ -478,7 +479,7 @@ def test_full_size_sampled(V, oracle, preset, head_aware, sparsity):
     dev = torch.device("cuda")
     q, k, v = synth.qkv(pre, device=dev)
     w = {n: t.to(dev) for n, t in synth.scorer_weights(pre).items()}
-    path = V.SparseAttention(pre.lat, cfgs, pre.heads, pre.d, w, sparsity=pre.sparsity)
+    path = V.SparseAttention(pre.lat, cfgs, pre.heads, pre.d, w, sparsity=pre.sparsity, keep_scores=True)
     if preset == "waver12b":  # 64x48x80 = 245,760 tokens; 95 % -> 96, 80 % -> 384, 98 % -> 38
         assert path.shape.n_tiles == 1920
         assert path.k == {0.95: 96, 0.80: 384, 0.98: 38}[round(pre.sparsity, 2)]
@@ -545,7 +546,7 @@ def test_wan13b_whole_call_vs_oracle(V, oracle):
     dev = torch.device("cuda")
     q, k, v = synth.qkv(pre, device=dev)
     w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, random_bias=True).items()}
-    path = V.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity)
+    path = V.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity, keep_scores=True)
     o = path(q, k, v)
     torch.cuda.synchronize()
     oq, ocnt, omask = oracle.tile_permute(u16(q), pre.lat, [pre.cfg])
@@ -636,7 +637,8 @@ def test_scorer_int8_ozaki_vs_fp64_dmma(V):
     heads = [0, 1, 2]
     q, k, v = synth.qkv(pre, heads=heads, device=dev)
     w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, heads=heads, random_bias=True).items()}
-    path = V.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev)
+    path = V.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev,
+                             keep_scores=True)
     path(q, k, v)
     eq = V.project(path.zq, w["w1q"], w["b1q"], w["w2q"], w["b2q"])
     ek = V.project(path.zk, w["w1k"], w["b1k"], w["w2k"], w["b2k"])
@@ -684,3 +686,31 @@ def test_degenerate_latents_token_path(V, oracle, lat, cfg, d):
     ov, _, _ = oracle.tile_permute(u16(v), lat, [cfg])
     o_t, _, _ = oracle.tile_permute(u16(o), lat, [cfg])
     check_attention(oracle, oq, ok_, ov, path.idx.cpu().numpy(), omask, o_t, tag=f"degenerate {lat}")
+
+
+@pytest.mark.parametrize("preset,hpc", [("waver12b", 0), ("wan14b", 3), ("wan1.3b", 5), ("wan1.3b", 1)])
+def test_select_fused_equals_score_then_topk(V, preset, hpc):
+    """veda_tile_select_pooled (phi for all heads, then S_pred and top-k per chunk of heads,
+    no [Hh, N_T, N_T] score tensor) gives the lists of
+    veda_tile_score_pooled -> veda_select_topk bit for bit, for any chunking (hpc = heads
+    per chunk, 0 = the library's 32 MB default: 2 heads at Waver), and the path object built
+    on it gives the same output."""
+    from paper_2605_30325_b200 import synth
+
+    pre = synth.PRESETS[preset]
+    dev = torch.device("cuda")
+    q, k, v = synth.qkv(pre, device=dev)
+    w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, random_bias=True).items()}
+    keep = V.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity, keep_scores=True)
+    o_keep = keep(q, k, v)
+    fused_idx = V.tile_select_pooled(keep.zq, keep.zk, keep.cnt, keep.scorer, keep.k, heads_per_chunk=hpc)
+    torch.cuda.synchronize()
+    assert torch.equal(fused_idx, keep.idx)
+    if hpc == 0:
+        fused = V.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity)
+        assert fused.scores is None
+        n0 = V.launch_count()
+        o = fused(q, k, v)
+        torch.cuda.synchronize()
+        assert V.launch_count() - n0 == fused.LAUNCHES_PER_CALL["tokens"]
+        assert torch.equal(fused.idx, keep.idx) and torch.equal(o.view(torch.int16), o_keep.view(torch.int16))

@@ -26,7 +26,8 @@ def case(V):
     q, k, v = synth.qkv(pre)
     dev = torch.device("cuda")
     w = {n: t.to(dev) for n, t in synth.scorer_weights(pre).items()}
-    path = V.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity, device=dev)
+    path = V.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity, device=dev,
+                             keep_scores=True)
     q, k, v = q.to(dev), k.to(dev), v.to(dev)
     o = path(q, k, v)
     torch.cuda.synchronize()
@@ -118,3 +119,24 @@ def test_out_of_range_lists_stay_inside_the_head(V, case):
     keep[0, 3] = False
     keep[1, 4] = False
     assert torch.equal(o2t[keep].view(torch.int16), ot[keep].view(torch.int16))
+
+
+def test_fused_select_debug_mode_flags_nonfinite_scores(V, case):
+    """Debug mode checks the pooled descriptors (and every score chunk) of
+    veda_tile_select_pooled: a NaN or inf descriptor gives VEDA_ERR_NONFINITE; valid inputs
+    give the same lists as the default mode; k outside [1, n_tiles] is VEDA_ERR_K_RANGE."""
+    pre, path, q, k, v, o = case
+    with pytest.raises(V.VedaError, match="VEDA_ERR_K_RANGE"):
+        V.tile_select_pooled(path.zq, path.zk, path.cnt, path.scorer, path.shape.n_tiles + 1)
+    prev = V.set_debug(1)
+    try:
+        idx = V.tile_select_pooled(path.zq, path.zk, path.cnt, path.scorer, path.k, heads_per_chunk=1)
+        torch.cuda.synchronize()
+        assert torch.equal(idx, path.idx)
+        for val in (float("nan"), float("inf")):
+            zk = path.zk.clone()
+            zk[1, 4, 7] = val
+            with pytest.raises(V.VedaError, match="VEDA_ERR_NONFINITE"):
+                V.tile_select_pooled(path.zq, zk, path.cnt, path.scorer, path.k, heads_per_chunk=1)
+    finally:
+        V.set_debug(prev)
