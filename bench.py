@@ -489,10 +489,11 @@ def run_ours(args):
                           "pool": {"bytes": pool_bytes, "ms": round(parts["pool"], 3),
                                    "gbs": round(pool_bytes / parts["pool"] / 1e6, 1),
                                    "frac": round(pool_bytes / parts["pool"] / 1e6 / peaks["hbm_gbs"], 3)},
-                          # phi + S_pred + top-k per 2-head chunk (veda_tile_select_pooled): the
-                          # [Hh, N_T, N_T] scores never exist; each chunk's 29.5 MB stays in L2
+                          # phi, then S_pred + top-k per chunk of heads (veda_tile_select_pooled):
+                          # the [Hh, N_T, N_T] score tensor never exists, only a chunk of it
                           "score_topk": {"ms": round(parts["score_topk"], 3),
-                                         "s_chunk_bytes": 2 * NT * NT * 4}} if "score_topk" in parts else
+                                         "s_chunk_bytes": veda.select_chunk_heads(Hh, NT) * NT * NT * 4,
+                                         "s_full_bytes": Hh * NT * NT * 4}} if "score_topk" in parts else
                          {"peak_gbs": peaks["hbm_gbs"],
                           "pool": {"bytes": pool_bytes, "ms": round(parts["pool"], 3),
                                    "gbs": round(pool_bytes / parts["pool"] / 1e6, 1),

@@ -353,14 +353,16 @@ veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32
 }
 
 // Steps 2 (phi, S_pred) + 3 (top-k) without a [Hh][N_T][N_T] score tensor: phi_q / phi_k
-// for all heads, then per chunk of heads the pair scores into a [chunk][N_T][N_T] scratch
-// that the top-k reads back straight away (chunk <= 32 MB by default, so the scores stay
-// in the 126 MB L2 between the two kernels and never round-trip through HBM).
+// and the digit images of e_q / e_k for all heads, then per chunk of heads the score GEMM
+// into a [chunk][N_T][N_T] scratch that the top-k reads back straight away.  Default chunk:
+// as many heads as fit 96 MB of fp32 scores (6 of Waver's 24: 88 MB instead of 354 MB);
+// smaller chunks cost the GEMM's and the top-k's wave tails (tools/select_bench.py:
+// 1 head 2.34 ms, 2 heads 2.04, 6 heads 1.87, the two-call form 1.89 at Waver).
 static int select_chunk_heads(int Hh, int NT, int heads_per_chunk)
 {
     if (heads_per_chunk > 0) return std::min(heads_per_chunk, Hh);
     const size_t per_head = (size_t)NT * NT * sizeof(float);
-    const size_t budget = (size_t)32 << 20;
+    const size_t budget = (size_t)96 << 20;
     return (int)std::max<size_t>(1, std::min<size_t>((size_t)Hh, budget / per_head));
 }
 
@@ -412,12 +414,14 @@ veda_status veda_tile_select_pooled(const float *zq, const float *zk, const int3
     if ((st = launch_ozaki_phi(zq, zk, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq, ek, oz_scratch,
                                S(stream))) != VEDA_OK)
         return st;
+    if ((st = launch_ozaki_split_e(eq, ek, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, oz_scratch, S(stream))) !=
+        VEDA_OK)
+        return st;
     const int hc = select_chunk_heads(Hh, n_tiles, heads_per_chunk);
     for (int h0 = 0; h0 < Hh; h0 += hc) {
         const int hn = std::min(hc, Hh - h0);
-        const size_t e0 = (size_t)h0 * n_tiles * w->d_lat;
-        if ((st = launch_ozaki_pair_scores(eq + e0, ek + e0, tile_count + (size_t)h0 * n_tiles, hn, n_tiles, w->d_in,
-                                           w->d_hidden, w->d_lat, s_chunk, oz_scratch, S(stream))) != VEDA_OK)
+        if ((st = launch_ozaki_score_gemm(tile_count, Hh, h0, hn, n_tiles, w->d_in, w->d_hidden, w->d_lat, s_chunk,
+                                          oz_scratch, S(stream))) != VEDA_OK)
             return st;
         if (debug_mode() && (st = debug_validate(S(stream), [&](uint32_t *f) {
                                  return launch_validate_scores(s_chunk, (int64_t)hn * n_tiles * n_tiles, f, S(stream));

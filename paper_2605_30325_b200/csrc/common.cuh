@@ -88,6 +88,10 @@ veda_status launch_ozaki_phi(const float *zq, const float *zk, int Hh, int NT, i
                              double *ek, void *scratch, cudaStream_t s);
 veda_status launch_ozaki_pair_scores(const double *eq, const double *ek, const int32_t *cnt, int Hh, int NT, int din,
                                      int dh, int dl, float *scores, void *scratch, cudaStream_t s);
+veda_status launch_ozaki_split_e(const double *eq, const double *ek, int Hh, int NT, int din, int dh, int dl,
+                                 void *scratch, cudaStream_t s);
+veda_status launch_ozaki_score_gemm(const int32_t *cnt, int Hh, int h0, int hn, int NT, int din, int dh, int dl,
+                                    float *scores, const void *scratch, cudaStream_t s);
 veda_status launch_target_scores(const uint16_t *q, const uint16_t *k, const uint32_t *mask, const float *lse,
                                  int Hh, int NT, int B, int d, float scale, float *out, cudaStream_t s);
 veda_status launch_permute_scalar(const float *x, int64_t hs, const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp,

@@ -666,10 +666,9 @@ veda_status launch_ozaki_phi(const float *zq, const float *zk, int Hh, int NT, i
     return VEDA_OK;
 }
 
-// S_pred = e_q e_k^T / sqrt(d'), -inf on empty key tiles, for Hh heads (pointers at the
-// first head); scratch >= ozaki_workspace(Hh, ...).
-veda_status launch_ozaki_pair_scores(const double *eq, const double *ek, const int32_t *cnt, int Hh, int NT, int din,
-                                     int dh, int dl, float *scores, void *scratch, cudaStream_t s)
+// Digit images of e_q (A) and e_k (B) for all Hh heads (scratch >= ozaki_workspace).
+veda_status launch_ozaki_split_e(const double *eq, const double *ek, int Hh, int NT, int din, int dh, int dl,
+                                 void *scratch, cudaStream_t s)
 {
     const size_t amax = img_a_bytes(NT, din, dh, dl);
     const size_t bmax = img_b_bytes(NT, din, dh, dl);
@@ -680,10 +679,36 @@ veda_status launch_ozaki_pair_scores(const double *eq, const double *ek, const i
     int32_t *eb = reinterpret_cast<int32_t *>(p);
     veda_status st;
     if ((st = oz::split_rows<double>(eq, NT, dl, dl, (int64_t)NT * dl, Hh, As, ea, oz::BM, s)) != VEDA_OK) return st;
-    if ((st = oz::split_rows<double>(ek, NT, dl, dl, (int64_t)NT * dl, Hh, Bs, eb, 96, s)) != VEDA_OK) return st;
+    return oz::split_rows<double>(ek, NT, dl, dl, (int64_t)NT * dl, Hh, Bs, eb, 96, s);
+}
+
+// S_pred = e_q e_k^T / sqrt(d'), -inf on empty key tiles, for heads [h0, h0 + hn) of the
+// Hh-head images launch_ozaki_split_e wrote (scores: the chunk's [hn][NT][NT]).
+veda_status launch_ozaki_score_gemm(const int32_t *cnt, int Hh, int h0, int hn, int NT, int din, int dh, int dl,
+                                    float *scores, const void *scratch, cudaStream_t s)
+{
+    const size_t amax = img_a_bytes(NT, din, dh, dl);
+    const size_t bmax = img_b_bytes(NT, din, dh, dl);
+    const char *p = static_cast<const char *>(scratch);
+    const int8_t *As = reinterpret_cast<const int8_t *>(p); p += align256((size_t)Hh * oz::NS * amax);
+    const int8_t *Bs = reinterpret_cast<const int8_t *>(p); p += align256((size_t)Hh * oz::NS * bmax);
+    const int32_t *ea = reinterpret_cast<const int32_t *>(p); p += align256((size_t)Hh * NT * 4);
+    const int32_t *eb = reinterpret_cast<const int32_t *>(p);
+    // per-head image strides (whole blocks of BM / 96 rows, 64-byte slabs of d_lat)
+    const size_t a_head = (size_t)oz::image_of(NT, dl, oz::BM).nblk * oz::BM * oz::NS * oz::kpad(dl);
+    const size_t b_head = (size_t)oz::image_of(NT, dl, 96).nblk * 96 * oz::NS * oz::kpad(dl);
     oz::GemmArgs a{};
-    a.ea = ea; a.eb = eb; a.cnt = cnt; a.C = scores; a.den = std::sqrt((double)dl);
-    return oz::gemm<96, oz::EPI_SCORE>(As, Bs, NT, NT, dl, Hh, a, s);
+    a.ea = ea + (size_t)h0 * NT; a.eb = eb + (size_t)h0 * NT; a.cnt = cnt + (size_t)h0 * NT;
+    a.C = scores; a.den = std::sqrt((double)dl);
+    return oz::gemm<96, oz::EPI_SCORE>(As + h0 * a_head, Bs + h0 * b_head, NT, NT, dl, hn, a, s);
+}
+
+veda_status launch_ozaki_pair_scores(const double *eq, const double *ek, const int32_t *cnt, int Hh, int NT, int din,
+                                     int dh, int dl, float *scores, void *scratch, cudaStream_t s)
+{
+    veda_status st = launch_ozaki_split_e(eq, ek, Hh, NT, din, dh, dl, scratch, s);
+    if (st != VEDA_OK) return st;
+    return launch_ozaki_score_gemm(cnt, Hh, 0, Hh, NT, din, dh, dl, scores, scratch, s);
 }
 
 // phi_q, phi_k and S_pred for all heads (the unfused form of veda_tile_score)

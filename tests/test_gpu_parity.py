@@ -693,7 +693,7 @@ def test_select_fused_equals_score_then_topk(V, preset, hpc):
     """veda_tile_select_pooled (phi for all heads, then S_pred and top-k per chunk of heads,
     no [Hh, N_T, N_T] score tensor) gives the lists of
     veda_tile_score_pooled -> veda_select_topk bit for bit, for any chunking (hpc = heads
-    per chunk, 0 = the library's 32 MB default: 2 heads at Waver), and the path object built
+    per chunk, 0 = the library's 96 MB default: 6 heads at Waver), and the path object built
     on it gives the same output."""
     from paper_2605_30325_b200 import synth
 
