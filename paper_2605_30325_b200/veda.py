@@ -718,14 +718,14 @@ class SparseAttention:
     @property
     def LAUNCHES_PER_CALL(self):
         """Kernel launches of one call.  Scorer (INT8 Ozaki): phi = per side 2 x (split rows,
-        split cols, GEMM) = 12; per chunk of heads 2 splits + the score GEMM (+ the top-k in
-        the fused select).  tokens: pool x2, phi, chunks x (splits, GEMM, top-k), attn (one
-        chunk with keep_scores); tiled: permute x3, pool x2, phi, 3, topk, attn, unpermute."""
-        phi = 12
+        split cols, GEMM) = 12; the digit splits of e_q / e_k = 2; per chunk of heads the
+        score GEMM + the top-k (one chunk with keep_scores: the full S, then select_topk).
+        tokens: pool x2, scorer, attn;  tiled: permute x3, pool x2, scorer, attn, unpermute."""
         nh = max(1, len(self.heads))
         chunks = 1 if self.keep_scores else -(-nh // select_chunk_heads(nh, self.shape.n_tiles,
                                                                          self.ws.heads_per_chunk))
-        return {"tokens": 2 + phi + 4 * chunks + 1, "tiled": 3 + 2 + phi + 3 + 1 + 1 + 1}
+        scorer = 12 + 2 + 2 * chunks
+        return {"tokens": 2 + scorer + 1, "tiled": 3 + 2 + scorer + 1 + 1}
 
     def run_host(self, q, k, v, out=None, heads_per_chunk: int = 0):
         """The same call on HOST tensors (veda_sparse_attention_host): q, k, v, out are
