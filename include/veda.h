@@ -99,6 +99,10 @@ typedef struct {
     int32_t d_in, d_hidden, d_lat;
     const float *w1q, *b1q, *w2q, *b2q;
     const float *w1k, *b1k, *w2k, *b2k;
+    /* optional (NULL: none): the device buffer veda_scorer_prepare filled from THESE
+     * weights for the same Hh; the scoring calls then skip splitting W1 and W2 on every
+     * call (inference weights are static).  Refill it if the weights change.        */
+    const void *prepared;
 } veda_scorer;
 
 /* ---- host helpers ----------------------------------------------------------- */
@@ -110,6 +114,15 @@ VEDA_API veda_status veda_tiled_shape_of(veda_latent lat, const veda_tile_cfg *c
 
 /* k = floor((1 - sparsity) * n_tiles + 1/2) clamped to [1, n_tiles] (reading R12). */
 VEDA_API int32_t veda_k_for_sparsity(int32_t n_tiles, double sparsity);
+
+/* Prepared scorer weights (phi's W1 and W2 of both sides as INT8 digit images + row
+ * exponents, the B operands of the Ozaki GEMMs, see veda_tile_score): bytes for Hh heads,
+ * and the fill (enqueued on stream; prepared is a caller-owned device buffer).  Results
+ * with and without w->prepared are bit-identical.                                    */
+VEDA_API veda_status veda_scorer_prepare_bytes(int32_t Hh, int32_t d, const veda_scorer *w /* host */,
+                                               size_t *bytes /* host */);
+VEDA_API veda_status veda_scorer_prepare(int32_t Hh, int32_t d, const veda_scorer *w /* host */, void *prepared,
+                                         size_t bytes, void *stream);
 
 /* Bytes of workspace veda_tile_score needs. */
 VEDA_API veda_status veda_tile_score_workspace(int32_t Hh, int32_t n_tiles, int32_t d,

@@ -298,6 +298,32 @@ veda_status veda_pair_scores(const double *eq, const double *ek, const int32_t *
     return launch_pair_scores(eq, ek, tile_count, Hh, n_tiles, d_lat, scores, S(stream));
 }
 
+veda_status veda_scorer_prepare_bytes(int32_t Hh, int32_t d, const veda_scorer *w, size_t *bytes)
+{
+    if (!w || !bytes) return fail(VEDA_ERR_NULL, "scorer_prepare_bytes: NULL pointer");
+    size_t unused = 0;
+    veda_status st = veda_tile_score_workspace(Hh, 1, d, w, &unused);  // the scorer's shape checks
+    if (st != VEDA_OK) return st;
+    *bytes = ozaki_prepared_bytes(Hh, w->d_in, w->d_hidden, w->d_lat);
+    return VEDA_OK;
+}
+
+veda_status veda_scorer_prepare(int32_t Hh, int32_t d, const veda_scorer *w, void *prepared, size_t bytes,
+                                void *stream)
+{
+    if (!w || !prepared) return fail(VEDA_ERR_NULL, "scorer_prepare: NULL pointer");
+    if (!w->w1q || !w->b1q || !w->w2q || !w->b2q || !w->w1k || !w->b1k || !w->w2k || !w->b2k)
+        return fail(VEDA_ERR_NULL, "scorer_prepare: NULL scorer weight");
+    size_t need = 0;
+    veda_status st = veda_scorer_prepare_bytes(Hh, d, w, &need);
+    if (st != VEDA_OK) return st;
+    if (bytes < need) return fail(VEDA_ERR_WORKSPACE, "scorer_prepare: buffer %zu < %zu", bytes, need);
+    if (!aligned16(prepared)) return fail(VEDA_ERR_ALIGN, "scorer_prepare: buffer not aligned");
+    if ((st = check_arch()) != VEDA_OK) return st;
+    const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
+    return launch_ozaki_prepare(wq, wk, Hh, w->d_in, w->d_hidden, w->d_lat, prepared, S(stream));
+}
+
 veda_status veda_tile_score(const uint16_t *q_tiled, const uint16_t *k_tiled, const int32_t *tile_count,
                             const uint32_t *slot_mask, int32_t Hh, int32_t n_tiles, int32_t B, int32_t d,
                             const veda_scorer *w, float *scores, void *workspace, size_t workspace_bytes,
@@ -322,7 +348,7 @@ veda_status veda_tile_score(const uint16_t *q_tiled, const uint16_t *k_tiled, co
     if ((st = veda_trippool(q_tiled, slot_mask, Hh, n_tiles, B, d, zq, stream)) != VEDA_OK) return st;
     if ((st = veda_trippool(k_tiled, slot_mask, Hh, n_tiles, B, d, zk, stream)) != VEDA_OK) return st;
     const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
-    return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq, ek,
+    return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, w->prepared, hid, eq, ek,
                               scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),
                               S(stream));
 }
@@ -347,7 +373,7 @@ veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32
     double *eq = reinterpret_cast<double *>(p); p += align256(rows * w->d_lat * sizeof(double));
     double *ek = reinterpret_cast<double *>(p);
     const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
-    return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq, ek,
+    return launch_ozaki_score(zq, zk, tile_count, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, w->prepared, hid, eq, ek,
                               scores, reinterpret_cast<char *>(ek) + align256(rows * w->d_lat * sizeof(double)),
                               S(stream));
 }
@@ -411,7 +437,7 @@ veda_status veda_tile_select_pooled(const float *zq, const float *zk, const int3
     void *oz_scratch = p;
     float *s_chunk = reinterpret_cast<float *>(static_cast<char *>(workspace) + score_ws);
     const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
-    if ((st = launch_ozaki_phi(zq, zk, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, hid, eq, ek, oz_scratch,
+    if ((st = launch_ozaki_phi(zq, zk, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, w->prepared, hid, eq, ek, oz_scratch,
                                S(stream))) != VEDA_OK)
         return st;
     if ((st = launch_ozaki_split_e(eq, ek, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, oz_scratch, S(stream))) !=

@@ -81,11 +81,14 @@ veda_status launch_tile_pool_tokens(const uint16_t *x, int64_t hs, int64_t ts, c
 // scorer GEMMs on the INT8 tensor cores (ozaki.cu); w_q / w_k = {w1, b1, w2, b2}
 size_t ozaki_workspace(int Hh, int NT, int din, int dh, int dl);
 veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *cnt, int Hh, int NT, int din, int dh,
-                               int dl, const float *const w_q[4], const float *const w_k[4], double *hidden,
-                               double *eq, double *ek, float *scores, void *scratch, cudaStream_t s);
+                               int dl, const float *const w_q[4], const float *const w_k[4], const void *prepared,
+                               double *hidden, double *eq, double *ek, float *scores, void *scratch, cudaStream_t s);
 veda_status launch_ozaki_phi(const float *zq, const float *zk, int Hh, int NT, int din, int dh, int dl,
-                             const float *const w_q[4], const float *const w_k[4], double *hidden, double *eq,
-                             double *ek, void *scratch, cudaStream_t s);
+                             const float *const w_q[4], const float *const w_k[4], const void *prepared,
+                             double *hidden, double *eq, double *ek, void *scratch, cudaStream_t s);
+size_t ozaki_prepared_bytes(int Hh, int din, int dh, int dl);
+veda_status launch_ozaki_prepare(const float *const w_q[4], const float *const w_k[4], int Hh, int din, int dh, int dl,
+                                 void *prepared, cudaStream_t s);
 veda_status launch_ozaki_pair_scores(const double *eq, const double *ek, const int32_t *cnt, int Hh, int NT, int din,
                                      int dh, int dl, float *scores, void *scratch, cudaStream_t s);
 veda_status launch_ozaki_split_e(const double *eq, const double *ek, int Hh, int NT, int din, int dh, int dl,

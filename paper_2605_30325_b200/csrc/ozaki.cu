@@ -631,11 +631,62 @@ size_t ozaki_workspace(int Hh, int NT, int din, int dh, int dl)
            align256((size_t)Hh * NT * 4) + align256((size_t)Hh * emax * 4);
 }
 
+// Prepared weights (veda_scorer_prepare): the digit images and row exponents of W1 and W2
+// of both sides, split once instead of on every call.  Layout for Hh heads (each region
+// 256-byte aligned): W1q image, W2q image, W1k image, W2k image (B operands: d_h rows in
+// blocks of 96 over d_in, d_lat rows in blocks of 64 over d_h), then the int32 exponents
+// e1q [Hh][d_h], e2q [Hh][d_lat], e1k, e2k.
+struct Prepared {
+    const int8_t *img[4];  // W1q, W2q, W1k, W2k
+    const int32_t *ex[4];
+};
+static size_t prep_img_bytes(int which, int din, int dh, int dl)  // per head
+{
+    const oz::Img m = (which & 1) ? oz::image_of(dl, dh, 64) : oz::image_of(dh, din, 96);
+    return (size_t)m.nblk * m.BR * oz::NS * m.nslab * oz::BKB;
+}
+size_t ozaki_prepared_bytes(int Hh, int din, int dh, int dl)
+{
+    size_t b = 0;
+    for (int i = 0; i < 4; ++i) b += align256((size_t)Hh * prep_img_bytes(i, din, dh, dl));
+    for (int i = 0; i < 4; ++i) b += align256((size_t)Hh * ((i & 1) ? dl : dh) * sizeof(int32_t));
+    return b;
+}
+static Prepared prepared_layout(const void *base, int Hh, int din, int dh, int dl)
+{
+    Prepared P;
+    const char *p = static_cast<const char *>(base);
+    for (int i = 0; i < 4; ++i) {
+        P.img[i] = reinterpret_cast<const int8_t *>(p);
+        p += align256((size_t)Hh * prep_img_bytes(i, din, dh, dl));
+    }
+    for (int i = 0; i < 4; ++i) {
+        P.ex[i] = reinterpret_cast<const int32_t *>(p);
+        p += align256((size_t)Hh * ((i & 1) ? dl : dh) * sizeof(int32_t));
+    }
+    return P;
+}
+veda_status launch_ozaki_prepare(const float *const w_q[4], const float *const w_k[4], int Hh, int din, int dh, int dl,
+                                 void *prepared, cudaStream_t s)
+{
+    const Prepared P = prepared_layout(prepared, Hh, din, dh, dl);
+    veda_status st;
+    for (int side = 0; side < 2; ++side) {
+        const float *const *w = side ? w_k : w_q;
+        int8_t *i1 = const_cast<int8_t *>(P.img[2 * side]), *i2 = const_cast<int8_t *>(P.img[2 * side + 1]);
+        int32_t *e1 = const_cast<int32_t *>(P.ex[2 * side]), *e2 = const_cast<int32_t *>(P.ex[2 * side + 1]);
+        if ((st = oz::split_cols<float>(w[0], dh, din, dh, (int64_t)din * dh, Hh, i1, e1, 96, s)) != VEDA_OK) return st;
+        if ((st = oz::split_cols<float>(w[2], dl, dh, dl, (int64_t)dh * dl, Hh, i2, e2, 64, s)) != VEDA_OK) return st;
+    }
+    return VEDA_OK;
+}
+
 // phi_q, phi_k (Eq. 6's MLPs) from pooled descriptors on the INT8 tensor cores.
 // hidden [Hh][NT][dh], eq / ek [Hh][NT][dl] are fp64 buffers; scratch >= ozaki_workspace.
+// prepared: the weights' images from launch_ozaki_prepare, or NULL (split here).
 veda_status launch_ozaki_phi(const float *zq, const float *zk, int Hh, int NT, int din, int dh, int dl,
-                             const float *const w_q[4], const float *const w_k[4], double *hidden, double *eq,
-                             double *ek, void *scratch, cudaStream_t s)
+                             const float *const w_q[4], const float *const w_k[4], const void *prepared,
+                             double *hidden, double *eq, double *ek, void *scratch, cudaStream_t s)
 {
     const size_t amax = img_a_bytes(NT, din, dh, dl);
     const size_t bmax = img_b_bytes(NT, din, dh, dl);
@@ -644,6 +695,8 @@ veda_status launch_ozaki_phi(const float *zq, const float *zk, int Hh, int NT, i
     int8_t *Bs = reinterpret_cast<int8_t *>(p); p += align256((size_t)Hh * oz::NS * bmax);
     int32_t *ea = reinterpret_cast<int32_t *>(p); p += align256((size_t)Hh * NT * 4);
     int32_t *eb = reinterpret_cast<int32_t *>(p);
+    Prepared P{};
+    if (prepared) P = prepared_layout(prepared, Hh, din, dh, dl);
     veda_status st;
     if ((st = phi_table_ready(s)) != VEDA_OK) return st;
     for (int side = 0; side < 2; ++side) {
@@ -652,16 +705,30 @@ veda_status launch_ozaki_phi(const float *zq, const float *zk, int Hh, int NT, i
         double *e = side ? ek : eq;
         // layer 1: pre-activation z W1 + b1
         if ((st = oz::split_rows<float>(z, NT, din, din, (int64_t)NT * din, Hh, As, ea, oz::BM, s)) != VEDA_OK) return st;
-        if ((st = oz::split_cols<float>(w[0], dh, din, dh, (int64_t)din * dh, Hh, Bs, eb, 96, s)) != VEDA_OK) return st;
+        const int8_t *b1 = Bs;
+        const int32_t *x1 = eb;
+        if (prepared) {
+            b1 = P.img[2 * side];
+            x1 = P.ex[2 * side];
+        } else if ((st = oz::split_cols<float>(w[0], dh, din, dh, (int64_t)din * dh, Hh, Bs, eb, 96, s)) != VEDA_OK) {
+            return st;
+        }
         oz::GemmArgs a{};
-        a.ea = ea; a.eb = eb; a.bias = w[1]; a.C = hidden;  // pre-activation z W1 + b1
-        if ((st = oz::gemm<96, oz::EPI_BIAS>(As, Bs, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
+        a.ea = ea; a.eb = x1; a.bias = w[1]; a.C = hidden;  // pre-activation z W1 + b1
+        if ((st = oz::gemm<96, oz::EPI_BIAS>(As, b1, NT, dh, din, Hh, a, s)) != VEDA_OK) return st;
         // layer 2: e = GELU(pre) W2 + b2 (the GELU is applied while splitting the rows)
         if ((st = oz::split_rows<double, true>(hidden, NT, dh, dh, (int64_t)NT * dh, Hh, As, ea, oz::BM, s)) != VEDA_OK)
             return st;
-        if ((st = oz::split_cols<float>(w[2], dl, dh, dl, (int64_t)dh * dl, Hh, Bs, eb, 64, s)) != VEDA_OK) return st;
-        a.bias = w[3]; a.C = e;
-        if ((st = oz::gemm<64, oz::EPI_BIAS>(As, Bs, NT, dl, dh, Hh, a, s)) != VEDA_OK) return st;
+        const int8_t *b2 = Bs;
+        const int32_t *x2 = eb;
+        if (prepared) {
+            b2 = P.img[2 * side + 1];
+            x2 = P.ex[2 * side + 1];
+        } else if ((st = oz::split_cols<float>(w[2], dl, dh, dl, (int64_t)dh * dl, Hh, Bs, eb, 64, s)) != VEDA_OK) {
+            return st;
+        }
+        a.eb = x2; a.bias = w[3]; a.C = e;
+        if ((st = oz::gemm<64, oz::EPI_BIAS>(As, b2, NT, dl, dh, Hh, a, s)) != VEDA_OK) return st;
     }
     return VEDA_OK;
 }
@@ -713,10 +780,10 @@ veda_status launch_ozaki_pair_scores(const double *eq, const double *ek, const i
 
 // phi_q, phi_k and S_pred for all heads (the unfused form of veda_tile_score)
 veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *cnt, int Hh, int NT, int din, int dh,
-                               int dl, const float *const w_q[4], const float *const w_k[4], double *hidden,
-                               double *eq, double *ek, float *scores, void *scratch, cudaStream_t s)
+                               int dl, const float *const w_q[4], const float *const w_k[4], const void *prepared,
+                               double *hidden, double *eq, double *ek, float *scores, void *scratch, cudaStream_t s)
 {
-    veda_status st = launch_ozaki_phi(zq, zk, Hh, NT, din, dh, dl, w_q, w_k, hidden, eq, ek, scratch, s);
+    veda_status st = launch_ozaki_phi(zq, zk, Hh, NT, din, dh, dl, w_q, w_k, prepared, hidden, eq, ek, scratch, s);
     if (st != VEDA_OK) return st;
     return launch_ozaki_pair_scores(eq, ek, cnt, Hh, NT, din, dh, dl, scores, scratch, s);
 }

@@ -221,6 +221,7 @@ veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k
                                               sh.NT, d, zk, nullptr, nullptr, cs)) != VEDA_OK)
                 return st;
             veda_scorer wc = *w;
+        wc.prepared = nullptr;  // prepared images are laid out for the whole head range
             const size_t o1 = (size_t)h0 * w->d_in * w->d_hidden, o2 = (size_t)h0 * w->d_hidden * w->d_lat;
             wc.w1q += o1; wc.w1k += o1; wc.b1q += (size_t)h0 * w->d_hidden; wc.b1k += (size_t)h0 * w->d_hidden;
             wc.w2q += o2; wc.w2k += o2; wc.b2q += (size_t)h0 * w->d_lat; wc.b2k += (size_t)h0 * w->d_lat;

@@ -33,7 +33,7 @@ EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_worksp
            "veda_tile_pool", "veda_sparse_attn_fwd_tokens", "veda_sparse_attn_fwd_tokens_units",
            "veda_tile_pool_heads", "veda_validate_index", "veda_validate_finite", "veda_set_debug",
            "veda_tile_pool_local", "veda_sparse_attn_fwd_tokens_local", "veda_tile_select_workspace",
-           "veda_tile_select_pooled"]
+           "veda_tile_select_pooled", "veda_scorer_prepare_bytes", "veda_scorer_prepare"]
 
 
 class VedaError(RuntimeError):
@@ -55,7 +55,7 @@ class TiledShape(ctypes.Structure):
 
 class Scorer(ctypes.Structure):
     _fields_ = [("d_in", ctypes.c_int32), ("d_hidden", ctypes.c_int32), ("d_lat", ctypes.c_int32)] + [
-        (n, ctypes.c_void_p) for n in ("w1q", "b1q", "w2q", "b2q", "w1k", "b1k", "w2k", "b2k")]
+        (n, ctypes.c_void_p) for n in ("w1q", "b1q", "w2q", "b2q", "w1k", "b1k", "w2k", "b2k", "prepared")]
 
 
 _lib = None
@@ -79,6 +79,8 @@ def load(path: str = LIB_PATH):
         "veda_tile_permute_pool": ([P, i64, i64, Latent, P, i32, i32, P, P, P, P, P], i32),
         "veda_tile_score_pooled": ([P, P, P, i32, i32, i32, P, P, P, sz, P], i32),
         "veda_tile_select_workspace": ([i32, i32, i32, P, i32, P], i32),
+        "veda_scorer_prepare_bytes": ([i32, i32, P, P], i32),
+        "veda_scorer_prepare": ([i32, i32, P, P, sz, P], i32),
         "veda_tile_select_pooled": ([P, P, P, i32, i32, i32, P, i32, i32, P, P, sz, P], i32),
         "veda_tile_score": ([P, P, P, P, i32, i32, i32, i32, P, P, P, sz, P], i32),
         "veda_select_topk": ([P, i32, i32, i32, P, P], i32),
@@ -336,6 +338,19 @@ def make_scorer(w: dict):
     dl = w["w2q"].shape[-1]
     sc = Scorer(din, dh, dl, *[w[n].data_ptr() for n in ("w1q", "b1q", "w2q", "b2q", "w1k", "b1k", "w2k", "b2k")])
     return sc
+
+
+def prepare_scorer(scorer: Scorer, Hh: int, d: int, device):
+    """Fill a device buffer with the scorer's weight digit images (veda_scorer_prepare) and
+    point ``scorer.prepared`` at it; returns the buffer (keep it alive with the scorer)."""
+    n = ctypes.c_size_t(0)
+    lib = load()
+    _check(lib.veda_scorer_prepare_bytes(Hh, d, ctypes.byref(scorer), ctypes.byref(n)), "scorer_prepare_bytes")
+    buf = torch.empty(n.value, dtype=torch.uint8, device=device)
+    scorer.prepared = None
+    _check(lib.veda_scorer_prepare(Hh, d, ctypes.byref(scorer), _ptr(buf), n.value, _stream()), "scorer_prepare")
+    scorer.prepared = buf.data_ptr()
+    return buf
 
 
 class ScoreWorkspace:
@@ -601,6 +616,8 @@ class SparseAttention:
             self.w_sub = {n: t[h0:h1] for n, t in scorer_weights.items()}
             if h1 > h0:
                 self.scorer = make_scorer(self.w_sub)
+        # W1 / W2 digit images once per object (static weights): no weight splits per call
+        self._prep_buf = prepare_scorer(self.scorer, len(self.heads), d, dev) if len(self.heads) else None
         if self.keep_scores:
             self.ws = ScoreWorkspace(max(1, len(self.heads)), NT, d, self.scorer, dev)
         else:
@@ -718,13 +735,14 @@ class SparseAttention:
     @property
     def LAUNCHES_PER_CALL(self):
         """Kernel launches of one call.  Scorer (INT8 Ozaki): phi = per side 2 x (split rows,
-        split cols, GEMM) = 12; the digit splits of e_q / e_k = 2; per chunk of heads the
+        split cols, GEMM) = 12, or 8 with prepared weights (no split cols: the object's
+        default); the digit splits of e_q / e_k = 2; per chunk of heads the
         score GEMM + the top-k (one chunk with keep_scores: the full S, then select_topk).
         tokens: pool x2, scorer, attn;  tiled: permute x3, pool x2, scorer, attn, unpermute."""
         nh = max(1, len(self.heads))
         chunks = 1 if self.keep_scores else -(-nh // select_chunk_heads(nh, self.shape.n_tiles,
                                                                          self.ws.heads_per_chunk))
-        scorer = 12 + 2 + 2 * chunks
+        scorer = (8 if self.scorer.prepared else 12) + 2 + 2 * chunks
         return {"tokens": 2 + scorer + 1, "tiled": 3 + 2 + scorer + 1 + 1}
 
     def run_host(self, q, k, v, out=None, heads_per_chunk: int = 0):

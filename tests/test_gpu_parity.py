@@ -714,3 +714,24 @@ def test_select_fused_equals_score_then_topk(V, preset, hpc):
         torch.cuda.synchronize()
         assert V.launch_count() - n0 == fused.LAUNCHES_PER_CALL["tokens"]
         assert torch.equal(fused.idx, keep.idx) and torch.equal(o.view(torch.int16), o_keep.view(torch.int16))
+
+
+@pytest.mark.parametrize("name", ["toy_b128", "mixed_cfgs", "b128_d64", "wan_slice"])
+def test_prepared_scorer_bit_identical(V, name):
+    """veda_scorer_prepare (W1 / W2 digit images split once) gives the same scores as
+    splitting the weights on every call, bit for bit, in both scoring entry points."""
+    c = Case(name, **CASES[name])
+    dev = torch.device("cuda")
+    w = {n: t.to(dev) for n, t in c.w.items()}
+    kw = dict(k=c.k_keep) if c.k_keep is not None else dict(sparsity=c.sparsity)
+    path = V.SparseAttention(c.lat, c.cfgs, c.Hh, c.d, w, keep_scores=True, **kw)
+    path(c.q.to(dev), c.k.to(dev), c.v.to(dev))
+    plain = V.make_scorer(w)
+    assert path.scorer.prepared and not plain.prepared
+    s_plain = V.tile_score_pooled(path.zq, path.zk, path.cnt, plain)
+    s_prep = V.tile_score_pooled(path.zq, path.zk, path.cnt, path.scorer)
+    i_plain = V.tile_select_pooled(path.zq, path.zk, path.cnt, plain, path.k)
+    i_prep = V.tile_select_pooled(path.zq, path.zk, path.cnt, path.scorer, path.k)
+    torch.cuda.synchronize()
+    assert torch.equal(s_plain.view(torch.int32), s_prep.view(torch.int32))
+    assert torch.equal(i_plain, i_prep) and torch.equal(i_prep, path.idx)
