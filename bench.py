@@ -52,6 +52,9 @@ def parse():
                     help="query tiles per step of the --impl reference arm (a different sample each step)")
     ap.add_argument("--ulysses-chunks", type=int, default=3,
                     help="head chunks of the overlapped Ulysses exchange (N > 1)")
+    ap.add_argument("--dist", action="store_true",
+                    help="take the multi-rank code path even at N = 1 (NCCL process group, max over ranks, "
+                         "the Ulysses exchange): lets a one-GPU box exercise what N > 1 runs")
     return ap.parse_args()
 
 
@@ -266,8 +269,25 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    multi = world > 1 or args.dist  # the multi-rank code path (NCCL group, Ulysses timing)
+    if multi:
+        if "MASTER_ADDR" not in os.environ:  # --dist without torchrun: a group of one
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        # NCCL may print its version banner on stdout when the communicator is created; the
+        # driver reads ONE JSON line from stdout, so route fd 1 to stderr until it exists
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     build.build()
     veda.load()
     veda.check_device()
@@ -290,7 +310,7 @@ def run_ours(args):
 
     def barrier():
         torch.cuda.synchronize()
-        if world > 1:
+        if multi:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -404,7 +424,7 @@ def run_ours(args):
     # optional Ulysses mode (N > 1): sequence-sharded inputs [N_r, Hh, d], all-to-all to
     # heads, local path, all-to-all back; its two exchanges are the only collectives
     ulysses_ms = None
-    if world > 1:
+    if multi:
         from paper_2605_30325_b200 import ulysses as uly
 
         del q, k, v, out
@@ -511,7 +531,7 @@ def run_ours(args):
             "clocks": clock,
         }
         print(json.dumps(result), flush=True)
-    if world > 1:
+    if multi:
         dist.barrier()
         dist.destroy_process_group()
     return 0
