@@ -735,3 +735,26 @@ def test_prepared_scorer_bit_identical(V, name):
     torch.cuda.synchronize()
     assert torch.equal(s_plain.view(torch.int32), s_prep.view(torch.int32))
     assert torch.equal(i_plain, i_prep) and torch.equal(i_prep, path.idx)
+
+
+@pytest.mark.parametrize("name", ["tiny", "mixed_cfgs", "b128_d64", "toy_b64_d128"])
+@pytest.mark.parametrize("which_k", ["one", "all", "path"])
+def test_select_fused_edge_cases(V, oracle, name, which_k):
+    """Fused score + top-k on the small cases (fully padded key tiles -> -inf scores, ragged
+    grids, B = 64, d = 64) at k = 1, k = N_T and the case's k, with one head per chunk and
+    with more heads per chunk than the call has: lists equal the oracle's top-k of the GPU's
+    own scores (bit-exact, ties -> lower index, ascending)."""
+    c = Case(name, **CASES[name])
+    dev = torch.device("cuda")
+    w = {n: t.to(dev) for n, t in c.w.items()}
+    kw = dict(k=c.k_keep) if c.k_keep is not None else dict(sparsity=c.sparsity)
+    path = V.SparseAttention(c.lat, c.cfgs, c.Hh, c.d, w, keep_scores=True, **kw)
+    path(c.q.to(dev), c.k.to(dev), c.v.to(dev))
+    NT = path.shape.n_tiles
+    kk = {"one": 1, "all": NT, "path": path.k}[which_k]
+    s = path.scores.cpu().numpy().astype(np.float64)
+    want = oracle.topk(s, kk)
+    for hpc in (1, c.Hh + 3):
+        got = V.tile_select_pooled(path.zq, path.zk, path.cnt, path.scorer, kk, heads_per_chunk=hpc)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), want), (name, kk, hpc)
