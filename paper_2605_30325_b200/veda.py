@@ -349,6 +349,7 @@ def prepare_scorer(scorer: Scorer, Hh: int, d: int, device):
     buf = torch.empty(n.value, dtype=torch.uint8, device=device)
     scorer.prepared = None
     _check(lib.veda_scorer_prepare(Hh, d, ctypes.byref(scorer), _ptr(buf), n.value, _stream()), "scorer_prepare")
+    torch.cuda.current_stream(device).synchronize()  # one-time setup: ready for calls on any stream
     scorer.prepared = buf.data_ptr()
     return buf
 
