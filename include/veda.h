@@ -189,6 +189,16 @@ VEDA_API veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int6
                                     veda_latent lat, const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh,
                                     int32_t d, float *z, int32_t *tile_count, uint32_t *slot_mask, void *stream);
 
+/* veda_tile_pool of Q and K in ONE launch (same strides, layout and tile configs): zq, zk
+ * [Hh][N_T][3d]; tile_count / slot_mask (may be NULL) from q -- identical for k.  The
+ * persistent pooling kernel streams both tensors' tiles, so the second tensor pays no
+ * launch gap or ramp-up; results are bit-identical to two veda_tile_pool calls.       */
+VEDA_API veda_status veda_tile_pool_qk(const uint16_t *q, const uint16_t *k, int64_t head_stride,
+                                       int64_t token_stride, veda_latent lat,
+                                       const veda_tile_cfg *cfg /* host [Hh] */, int32_t Hh, int32_t d,
+                                       float *zq, float *zk, int32_t *tile_count, uint32_t *slot_mask,
+                                       void *stream);
+
 /* veda_tile_pool for the heads [head_begin, head_end) of an Hh-head call: the padded grid
  * (hence n_tiles and every tile) is the whole call's -- the lcm of ALL Hh heads' tile
  * extents -- and z / tile_count / slot_mask are the whole call's arrays, of which only the

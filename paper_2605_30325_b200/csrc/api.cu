@@ -525,6 +525,30 @@ veda_status veda_tile_pool(const uint16_t *x, int64_t head_stride, int64_t token
                                    sh.NT, d, z, tile_count, slot_mask, S(stream));
 }
 
+veda_status veda_tile_pool_qk(const uint16_t *q, const uint16_t *k, int64_t head_stride, int64_t token_stride,
+                              veda_latent lat, const veda_tile_cfg *cfg, int32_t Hh, int32_t d, float *zq, float *zk,
+                              int32_t *tile_count, uint32_t *slot_mask, void *stream)
+{
+    if (!q || !k || !zq || !zk) return fail(VEDA_ERR_NULL, "tile_pool_qk: NULL pointer");
+    if (d != 64 && d != 128) return fail(VEDA_ERR_SHAPE, "tile_pool_qk: d=%d unsupported", d);
+    if (!aligned16(q) || !aligned16(k) || (head_stride % 8) || (token_stride % 8))
+        return fail(VEDA_ERR_ALIGN, "tile_pool_qk: pointers/strides must be 16-byte aligned");
+    Shape sh;
+    HeadCfgs hc;
+    veda_status st = shape_of(lat, cfg, Hh, &sh, &hc);  // argument errors before any device call
+    if (st != VEDA_OK) return st;
+    if ((st = check_arch()) != VEDA_OK) return st;
+    if (debug_mode() && (st = debug_validate(S(stream), [&](uint32_t *f) {
+                             const int64_t n = (int64_t)lat.t * lat.h * lat.w;
+                             veda_status e = launch_validate_finite(q, head_stride, token_stride, Hh, n, d, f, S(stream));
+                             if (e == VEDA_OK) e = launch_validate_finite(k, head_stride, token_stride, Hh, n, d, f, S(stream));
+                             return e;
+                         })) != VEDA_OK)
+        return st;
+    return launch_tile_pool_tokens2(q, k, head_stride, token_stride, hc, Hh, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w,
+                                    sh.B, sh.NT, d, zq, zk, tile_count, slot_mask, S(stream));
+}
+
 static veda_status tile_pool_range_impl(const uint16_t *x, int64_t head_stride, int64_t token_stride, veda_latent lat,
                                         const veda_tile_cfg *cfg, int32_t Hh, int32_t d, int32_t head_begin,
                                         int32_t head_end, float *z, int32_t *tile_count, uint32_t *slot_mask,

@@ -78,6 +78,10 @@ veda_status launch_sparse_attn_tok(const uint16_t *q, const uint16_t *k, const u
 veda_status launch_tile_pool_tokens(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfgs &cf, int Hh, int Tp,
                                     int Hp, int Wp, int T, int H, int W, int B, int NT, int d, float *z,
                                     int32_t *cnt, uint32_t *mask, cudaStream_t s);
+// Q and K pooled by one launch (same strides, same grid): z, z2 for x, x2; cnt / mask from x
+veda_status launch_tile_pool_tokens2(const uint16_t *x, const uint16_t *x2, int64_t hs, int64_t ts, const HeadCfgs &cf,
+                                     int Hh, int Tp, int Hp, int Wp, int T, int H, int W, int B, int NT, int d,
+                                     float *z, float *z2, int32_t *cnt, uint32_t *mask, cudaStream_t s);
 // scorer GEMMs on the INT8 tensor cores (ozaki.cu); w_q / w_k = {w1, b1, w2, b2}
 size_t ozaki_workspace(int Hh, int NT, int din, int dh, int dl);
 veda_status launch_ozaki_score(const float *zq, const float *zk, const int32_t *cnt, int Hh, int NT, int din, int dh,

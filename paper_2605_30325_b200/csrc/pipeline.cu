@@ -215,10 +215,8 @@ veda_status veda_sparse_attention_host(const uint16_t *q_host, const uint16_t *k
             VEDA_CU(cudaStreamWaitEvent(cs, ev_h2d[c], 0));
             HeadCfgs hcf;
             for (int h = 0; h < hn; ++h) { hcf.pt[h] = all.pt[h0 + h]; hcf.ph[h] = all.ph[h0 + h]; hcf.pw[h] = all.pw[h0 + h]; }
-            if ((st = launch_tile_pool_tokens(in[0], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
-                                              sh.NT, d, zq, cnt, mask, cs)) != VEDA_OK ||
-                (st = launch_tile_pool_tokens(in[1], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w, sh.B,
-                                              sh.NT, d, zk, nullptr, nullptr, cs)) != VEDA_OK)
+            if ((st = launch_tile_pool_tokens2(in[0], in[1], dhs, dts, hcf, hn, sh.Tp, sh.Hp, sh.Wp, lat.t, lat.h, lat.w,
+                                               sh.B, sh.NT, d, zq, zk, cnt, mask, cs)) != VEDA_OK)
                 return st;
             veda_scorer wc = *w;
         wc.prepared = nullptr;  // prepared images are laid out for the whole head range

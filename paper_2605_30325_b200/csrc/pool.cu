@@ -36,7 +36,9 @@ constexpr int PTHREADS = 32 + 32 * PWARPS;
 
 struct PoolParams {
     CUtensorMap map[PMAXC];
-    int T, H, W, NT, units;  // units = heads_in_launch * NT
+    CUtensorMap map2[PMAXC];  // second tensor (K) of a two-tensor launch (ntensor == 2)
+    int T, H, W, NT, units;  // units = heads_in_launch * NT (per tensor)
+    int ntensor;             // 1, or 2: units [units, 2 units) are the second tensor's tiles
     int tok_major;
     uint8_t pt[PMAXC], ph[PMAXC], pw[PMAXC];
     uint32_t nbw[PMAXC], nbhw[PMAXC], mbw[PMAXC], mbhw[PMAXC];
@@ -84,7 +86,8 @@ struct PGeo {
 
 template <int D, int BT>
 __global__ void __launch_bounds__(PTHREADS, 1) pool_tma_kernel(const __grid_constant__ PoolParams pp,
-                                                               float *__restrict__ z, int32_t *__restrict__ cnt,
+                                                               float *__restrict__ z, float *__restrict__ z2,
+                                                               int32_t *__restrict__ cnt,
                                                                uint32_t *__restrict__ mask)
 {
     using G = PGeo<D, BT>;
@@ -105,7 +108,8 @@ __global__ void __launch_bounds__(PTHREADS, 1) pool_tma_kernel(const __grid_cons
     }
     __syncthreads();
     const int grid = gridDim.x;
-    const int ntile = (pp.units - (int)blockIdx.x + grid - 1) / grid;  // tiles of this CTA: n*grid + blockIdx.x
+    const int all = pp.units * pp.ntensor;
+    const int ntile = (all - (int)blockIdx.x + grid - 1) / grid;  // tiles of this CTA: n*grid + blockIdx.x
     if (warp == 0) {
         // ------------------------------------------------ producer: one TMA box per tile
         if (lane == 0) {
@@ -113,13 +117,15 @@ __global__ void __launch_bounds__(PTHREADS, 1) pool_tma_kernel(const __grid_cons
                 const int st = n % G::NST;
                 const uint32_t ph = (uint32_t)(n / G::NST) & 1u;
                 mbar_wait(P_EMPTY(st), ph ^ 1u);
-                const int u = n * grid + (int)blockIdx.x, h = u / pp.NT, i = u - h * pp.NT;
+                const int ua = n * grid + (int)blockIdx.x, second = ua >= pp.units;
+                const int u = ua - (second ? pp.units : 0), h = u / pp.NT, i = u - h * pp.NT;
                 const Org o = origin(pp, h, i);
+                const CUtensorMap *mp = second ? &pp.map2[o.c] : &pp.map[o.c];
                 mbar_expect_tx(P_FULL(st), G::TILE);
                 if (pp.tok_major)
-                    tma_load_5d(sRing + st * G::TILE, &pp.map[o.c], 0, h, o.w0, o.h0, o.t0, P_FULL(st));
+                    tma_load_5d(sRing + st * G::TILE, mp, 0, h, o.w0, o.h0, o.t0, P_FULL(st));
                 else
-                    tma_load_5d(sRing + st * G::TILE, &pp.map[o.c], 0, o.w0, o.h0, o.t0, h, P_FULL(st));
+                    tma_load_5d(sRing + st * G::TILE, mp, 0, o.w0, o.h0, o.t0, h, P_FULL(st));
             }
         }
         __syncwarp();
@@ -134,7 +140,8 @@ __global__ void __launch_bounds__(PTHREADS, 1) pool_tma_kernel(const __grid_cons
     uint8_t *xch = smem + G::NST * G::TILE + 2 * G::NST * 8 + (size_t)grp * D * 16;
     for (int n = grp; n < ntile; n += G::NG) {
         const int st = n % G::NST;
-        const int u = n * grid + (int)blockIdx.x, h = u / pp.NT, i = u - h * pp.NT;
+        const int ua = n * grid + (int)blockIdx.x, second = ua >= pp.units;
+        const int u = ua - (second ? pp.units : 0), h = u / pp.NT, i = u - h * pp.NT;
         const Org o = origin(pp, h, i);
         const int pw = pp.pw[o.c], lpw = __ffs(pw) - 1, lphw = lpw + __ffs(pp.ph[o.c]) - 1;
         // slot mask of the tile: bit r set iff row r (dt, dh, dw raster) is a real token
@@ -210,7 +217,7 @@ __global__ void __launch_bounds__(PTHREADS, 1) pool_tma_kernel(const __grid_cons
         __syncwarp();
         if (lane == 0) mbar_arrive(P_EMPTY(st));  // this warp is done with the stage
         if (rh != 0) continue;
-        float *zz = z + (size_t)u * 3 * D + 2 * j;
+        float *zz = (second ? z2 : z) + (size_t)u * 3 * D + 2 * j;
         if (count == 0) {
             *reinterpret_cast<float2 *>(zz) = make_float2(0.f, 0.f);
             *reinterpret_cast<float2 *>(zz + D) = make_float2(0.f, 0.f);
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(PTHREADS, 1) pool_tma_kernel(const __grid_cons
             *reinterpret_cast<float2 *>(zz + D) = make_float2(max0, max1);
             *reinterpret_cast<float2 *>(zz + 2 * D) = make_float2(min0, min1);
         }
-        if (gw == 0 && lane < MW) {  // (rh == 0 here)
+        if (gw == 0 && lane < MW && !second) {  // (rh == 0 here); the counts / masks come from the first tensor
             uint32_t wv = mw[0];
 #pragma unroll
             for (int w = 1; w < MW; ++w)
@@ -234,8 +241,9 @@ __global__ void __launch_bounds__(PTHREADS, 1) pool_tma_kernel(const __grid_cons
 }
 
 template <int D, int BT>
-veda_status launch_pool(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfgs &cf, int Hh, int Hp, int Wp,
-                        int T, int H, int W, int NT, float *z, int32_t *cnt, uint32_t *mask, cudaStream_t s)
+veda_status launch_pool(const uint16_t *x, const uint16_t *x2, int64_t hs, int64_t ts, const HeadCfgs &cf, int Hh,
+                        int Hp, int Wp, int T, int H, int W, int NT, float *z, float *z2, int32_t *cnt,
+                        uint32_t *mask, cudaStream_t s)
 {
     using G = PGeo<D, BT>;
     cudaError_t e = cudaFuncSetAttribute(pool_tma_kernel<D, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
@@ -262,6 +270,9 @@ veda_status launch_pool(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfg
             if ((st = make_tmap_tile_tokens(&pp.map[c], x + (size_t)h0 * hs, hs, ts, hn, T, H, W, D, pp.pt[c], pp.ph[c],
                                             pp.pw[c], &tm, D, false)) != VEDA_OK)
                 return st;
+            if (x2 && (st = make_tmap_tile_tokens(&pp.map2[c], x2 + (size_t)h0 * hs, hs, ts, hn, T, H, W, D, pp.pt[c],
+                                                  pp.ph[c], pp.pw[c], &tm, D, false)) != VEDA_OK)
+                return st;
             pp.nbw[c] = (uint32_t)(Wp / pp.pw[c]);
             pp.nbhw[c] = (uint32_t)((Hp / pp.ph[c]) * (Wp / pp.pw[c]));
             auto magic = [](uint32_t n) {
@@ -272,11 +283,12 @@ veda_status launch_pool(const uint16_t *x, int64_t hs, int64_t ts, const HeadCfg
             pp.mbhw[c] = magic(pp.nbhw[c]);
         }
         pp.T = T; pp.H = H; pp.W = W; pp.NT = NT; pp.units = hn * NT; pp.tok_major = tm;
+        pp.ntensor = x2 ? 2 : 1;
         const int nsm = num_sms();
-        const int grid = pp.units < nsm ? pp.units : nsm;
+        const int grid = pp.units * pp.ntensor < nsm ? pp.units * pp.ntensor : nsm;
         pool_tma_kernel<D, BT><<<grid, PTHREADS, G::SMEM, s>>>(
-            pp, z + (size_t)h0 * NT * 3 * D, cnt ? cnt + (size_t)h0 * NT : nullptr,
-            mask ? mask + (size_t)h0 * NT * MW : nullptr);
+            pp, z + (size_t)h0 * NT * 3 * D, z2 ? z2 + (size_t)h0 * NT * 3 * D : nullptr,
+            cnt ? cnt + (size_t)h0 * NT : nullptr, mask ? mask + (size_t)h0 * NT * MW : nullptr);
         count_launch();
         if ((st = check_launch("tile_pool")) != VEDA_OK) return st;
         h0 = h1;
@@ -290,6 +302,13 @@ veda_status launch_tile_pool_tokens(const uint16_t *x, int64_t hs, int64_t ts, c
                                     int Hp, int Wp, int T, int H, int W, int B, int NT, int d, float *z,
                                     int32_t *cnt, uint32_t *mask, cudaStream_t s)
 {
+    return launch_tile_pool_tokens2(x, nullptr, hs, ts, cf, Hh, Tp, Hp, Wp, T, H, W, B, NT, d, z, nullptr, cnt, mask, s);
+}
+
+veda_status launch_tile_pool_tokens2(const uint16_t *x, const uint16_t *x2, int64_t hs, int64_t ts, const HeadCfgs &cf,
+                                     int Hh, int Tp, int Hp, int Wp, int T, int H, int W, int B, int NT, int d,
+                                     float *z, float *z2, int32_t *cnt, uint32_t *mask, cudaStream_t s)
+{
     (void)Tp;
     // a stride that is never used (one token, or one head) may equal the other one; give it
     // a distinct value so the 5-D tensor map gets a well-ordered dimension set
@@ -301,10 +320,10 @@ veda_status launch_tile_pool_tokens(const uint16_t *x, int64_t hs, int64_t ts, c
         else
             return fail(VEDA_ERR_ALIGN, "tile_pool: head_stride == token_stride");
     }
-    if (d == 128 && B == 128) return launch_pool<128, 128>(x, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, z, cnt, mask, s);
-    if (d == 128 && B == 64) return launch_pool<128, 64>(x, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, z, cnt, mask, s);
-    if (d == 64 && B == 128) return launch_pool<64, 128>(x, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, z, cnt, mask, s);
-    if (d == 64 && B == 64) return launch_pool<64, 64>(x, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, z, cnt, mask, s);
+    if (d == 128 && B == 128) return launch_pool<128, 128>(x, x2, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, z, z2, cnt, mask, s);
+    if (d == 128 && B == 64) return launch_pool<128, 64>(x, x2, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, z, z2, cnt, mask, s);
+    if (d == 64 && B == 128) return launch_pool<64, 128>(x, x2, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, z, z2, cnt, mask, s);
+    if (d == 64 && B == 64) return launch_pool<64, 64>(x, x2, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, z, z2, cnt, mask, s);
     return fail(VEDA_ERR_SHAPE, "tile_pool: unsupported B=%d d=%d", B, d);
 }
 

@@ -33,7 +33,7 @@ EXPORTS = ["veda_tiled_shape_of", "veda_k_for_sparsity", "veda_tile_score_worksp
            "veda_tile_pool", "veda_sparse_attn_fwd_tokens", "veda_sparse_attn_fwd_tokens_units",
            "veda_tile_pool_heads", "veda_validate_index", "veda_validate_finite", "veda_set_debug",
            "veda_tile_pool_local", "veda_sparse_attn_fwd_tokens_local", "veda_tile_select_workspace",
-           "veda_tile_select_pooled", "veda_scorer_prepare_bytes", "veda_scorer_prepare"]
+           "veda_tile_select_pooled", "veda_scorer_prepare_bytes", "veda_scorer_prepare", "veda_tile_pool_qk"]
 
 
 class VedaError(RuntimeError):
@@ -97,6 +97,7 @@ def load(path: str = LIB_PATH):
         "veda_sparse_attention_host_workspace": ([Latent, P, i32, i32, i32, P, i32, P], i32),
         "veda_sparse_attention_host": ([P, P, P, i64, i64, Latent, P, i32, i32, i32, P, i32, P, P, sz, P], i32),
         "veda_tile_pool": ([P, i64, i64, Latent, P, i32, i32, P, P, P, P], i32),
+        "veda_tile_pool_qk": ([P, P, i64, i64, Latent, P, i32, i32, P, P, P, P, P], i32),
         "veda_tile_pool_heads": ([P, i64, i64, Latent, P, i32, i32, i32, i32, P, P, P, P], i32),
         "veda_sparse_attn_fwd_tokens": ([P, P, P, i64, i64, Latent, P, i32, i32, P, P, i32, f32, P, i64, i64, P, P],
                                         i32),
@@ -452,6 +453,22 @@ def sparse_attn_fwd(q_tiled, k_tiled, v_tiled, idx, slot_mask, scale: float = 0.
     return (out, lse) if want_lse else out
 
 
+def tile_pool_qk(q: torch.Tensor, k: torch.Tensor, lat, cfgs):
+    """TripPool of Q and K in one launch (veda_tile_pool_qk).  Returns (zq, zk, tile_count,
+    slot_mask)."""
+    _need_cuda(q, k)
+    assert q.dtype == torch.bfloat16 and q.stride() == k.stride() and q.shape == k.shape and q.stride(2) == 1
+    Hh, N, d = q.shape
+    sh = tiled_shape(lat, cfgs, Hh)
+    zq = torch.empty((Hh, sh.n_tiles, 3 * d), dtype=torch.float32, device=q.device)
+    zk = torch.empty_like(zq)
+    cnt = torch.empty((Hh, sh.n_tiles), dtype=torch.int32, device=q.device)
+    mask = torch.empty((Hh, sh.n_tiles, sh.B // 32), dtype=torch.int32, device=q.device)
+    _check(load().veda_tile_pool_qk(_ptr(q), _ptr(k), q.stride(0), q.stride(1), Latent(*lat), _cfg_array(cfgs, Hh),
+                                    Hh, d, _ptr(zq), _ptr(zk), _ptr(cnt), _ptr(mask), _stream()), "tile_pool_qk")
+    return zq, zk, cnt, mask
+
+
 def tile_pool(x: torch.Tensor, lat, cfgs, z=None, meta=True):
     """TripPool of every tile of x [Hh, N, d] read straight from token order (veda_tile_pool).
     Returns (z [Hh, N_T, 3d] fp32, tile_count | None, slot_mask | None)."""
@@ -655,11 +672,10 @@ class SparseAttention:
             if not (k.stride() == q.stride() and v.stride() == q.stride()):
                 raise VedaError("q, k, v must share strides")
             h0, h1 = self.heads.start, self.heads.stop
-            if self.units is None:
-                _check(lib.veda_tile_pool(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, _ptr(self.zq),
-                                          _ptr(self.cnt), _ptr(self.mask), s), "tile_pool(q)")
-                _check(lib.veda_tile_pool(_ptr(k), k.stride(0), k.stride(1), lat, cfg, Hh, d, _ptr(self.zk), None,
-                                          None, s), "tile_pool(k)")
+            if self.units is None:  # Q and K in one pooling launch
+                _check(lib.veda_tile_pool_qk(_ptr(q), _ptr(k), q.stride(0), q.stride(1), lat, cfg, Hh, d,
+                                             _ptr(self.zq), _ptr(self.zk), _ptr(self.cnt), _ptr(self.mask), s),
+                       "tile_pool_qk")
             elif self.head_range is not None:  # head-shard tensors, the whole call's padded grid
                 _check(lib.veda_tile_pool_local(_ptr(q), q.stride(0), q.stride(1), lat, cfg, Hh, d, h0, h1,
                                                 _ptr(self.zq), _ptr(self.cnt), _ptr(self.mask), s), "tile_pool_local(q)")
@@ -744,7 +760,8 @@ class SparseAttention:
         chunks = 1 if self.keep_scores else -(-nh // select_chunk_heads(nh, self.shape.n_tiles,
                                                                          self.ws.heads_per_chunk))
         scorer = (8 if self.scorer.prepared else 12) + 2 + 2 * chunks
-        return {"tokens": 2 + scorer + 1, "tiled": 3 + 2 + scorer + 1 + 1}
+        pool = 1 if self.units is None else 2  # Q and K in one launch on the whole-call path
+        return {"tokens": pool + scorer + 1, "tiled": 3 + 2 + scorer + 1 + 1}
 
     def run_host(self, q, k, v, out=None, heads_per_chunk: int = 0):
         """The same call on HOST tensors (veda_sparse_attention_host): q, k, v, out are

@@ -758,3 +758,19 @@ def test_select_fused_edge_cases(V, oracle, name, which_k):
         got = V.tile_select_pooled(path.zq, path.zk, path.cnt, path.scorer, kk, heads_per_chunk=hpc)
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), want), (name, kk, hpc)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_tile_pool_qk_equals_two_pools(V, name):
+    """veda_tile_pool_qk (Q and K through one persistent launch) is bit-identical to two
+    veda_tile_pool calls: z of both tensors, tile counts and slot masks."""
+    c = Case(name, **CASES[name])
+    dev = torch.device("cuda")
+    q, k = c.q.to(dev), c.k.to(dev)
+    zq, zk, cnt, mask = V.tile_pool_qk(q, k, c.lat, c.cfgs)
+    zq1, cnt1, mask1 = V.tile_pool(q, c.lat, c.cfgs)
+    zk1, _, _ = V.tile_pool(k, c.lat, c.cfgs, meta=False)
+    torch.cuda.synchronize()
+    for a, b in ((zq, zq1), (zk, zk1)):
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    assert torch.equal(cnt, cnt1) and torch.equal(mask, mask1)
