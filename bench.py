@@ -512,7 +512,8 @@ def run_ours(args):
                           # phi, then S_pred + top-k per chunk of heads (veda_tile_select_pooled):
                           # the [Hh, N_T, N_T] score tensor never exists, only a chunk of it
                           "score_topk": {"ms": round(parts["score_topk"], 3),
-                                         "s_chunk_bytes": veda.select_chunk_heads(Hh, NT) * NT * NT * 4,
+                                         "s_scratch_bytes": (2 if veda.select_chunk_heads(Hh, NT) < Hh else 1)
+                                         * veda.select_chunk_heads(Hh, NT) * NT * NT * 4,
                                          "s_full_bytes": Hh * NT * NT * 4}} if "score_topk" in parts else
                          {"peak_gbs": peaks["hbm_gbs"],
                           "pool": {"bytes": pool_bytes, "ms": round(parts["pool"], 3),

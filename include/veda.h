@@ -316,9 +316,11 @@ VEDA_API veda_status veda_tile_score_pooled(const float *zq, const float *zk, co
  * kernel-level fusion to reduce mask preparation overhead"): the kept-tile lists idx
  * [Hh][N_T][k] straight from the pooled descriptors, with no [Hh][N_T][N_T] score tensor.
  * phi_q / phi_k (Eq. 6) run for all heads; then, per chunk of heads_per_chunk heads
- * (0: as many as fit 96 MB of fp32 scores -- 6 of Waver's 24), S_pred (Eq. 6) is written
+ * (0: as many as fit 48 MB of fp32 scores -- 3 of Waver's 24), S_pred (Eq. 6) is written
  * to a chunk-sized scratch in the workspace and the top-k of veda_select_topk
- * reads it straight back.  idx is bit-identical to
+ * reads it back; with several chunks the scratch is double-
+ * buffered and the top-k of chunk c runs on a library side stream while the score GEMM
+ * of chunk c+1 runs on `stream` (the caller's stream is made to wait for the last one).  idx is bit-identical to
  * veda_tile_score_pooled followed by veda_select_topk for any chunking.
  * Errors: VEDA_ERR_K_RANGE (k outside [1, n_tiles]), VEDA_ERR_WORKSPACE, as
  * veda_tile_score_pooled otherwise; debug mode also checks every score chunk.       */

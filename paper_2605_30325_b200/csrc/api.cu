@@ -8,6 +8,7 @@
 
 #include <atomic>
 #include <algorithm>
+#include <vector>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -380,17 +381,21 @@ veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32
 
 // Steps 2 (phi, S_pred) + 3 (top-k) without a [Hh][N_T][N_T] score tensor: phi_q / phi_k
 // and the digit images of e_q / e_k for all heads, then per chunk of heads the score GEMM
-// into a [chunk][N_T][N_T] scratch that the top-k reads back straight away.  Default chunk:
-// as many heads as fit 96 MB of fp32 scores (6 of Waver's 24: 88 MB instead of 354 MB);
-// smaller chunks cost the GEMM's and the top-k's wave tails (tools/select_bench.py:
-// 1 head 2.34 ms, 2 heads 2.04, 6 heads 1.87, the two-call form 1.89 at Waver).
+// into a [chunk][N_T][N_T] scratch that the top-k reads back.  Default chunk: as many heads
+// as fit 48 MB of fp32 scores (3 of Waver's 24), double-buffered (88 MB instead of 354 MB),
+// the top-k of chunk c on a side stream beside the score GEMM of chunk c+1
+// (tools/select_bench.py at Waver: 1.71 ms vs 1.59 for the two-call form with the full S).
 static int select_chunk_heads(int Hh, int NT, int heads_per_chunk)
 {
     if (heads_per_chunk > 0) return std::min(heads_per_chunk, Hh);
     const size_t per_head = (size_t)NT * NT * sizeof(float);
-    const size_t budget = (size_t)96 << 20;
+    const size_t budget = (size_t)48 << 20;
     return (int)std::max<size_t>(1, std::min<size_t>((size_t)Hh, budget / per_head));
 }
+
+// score scratch buffers: one chunk, or two (double-buffered between the score GEMM on the
+// caller's stream and the top-k on a side stream) when the call has several chunks
+static int select_buffers(int Hh, int hc) { return Hh > hc ? 2 : 1; }
 
 veda_status veda_tile_select_workspace(int32_t Hh, int32_t n_tiles, int32_t d, const veda_scorer *w,
                                        int32_t heads_per_chunk, size_t *bytes)
@@ -400,7 +405,22 @@ veda_status veda_tile_select_workspace(int32_t Hh, int32_t n_tiles, int32_t d, c
     if (st != VEDA_OK) return st;
     if (heads_per_chunk < 0) return fail(VEDA_ERR_SHAPE, "tile_select_workspace: heads_per_chunk=%d < 0", heads_per_chunk);
     const int hc = select_chunk_heads(Hh, n_tiles, heads_per_chunk);
-    *bytes = b + align256((size_t)hc * n_tiles * n_tiles * sizeof(float));
+    *bytes = b + select_buffers(Hh, hc) * align256((size_t)hc * n_tiles * n_tiles * sizeof(float));
+    return VEDA_OK;
+}
+
+// per-device side stream of veda_tile_select_pooled (the top-k of chunk c runs on it while
+// the score GEMM of chunk c+1 runs on the caller's stream)
+static veda_status select_side_stream(cudaStream_t *out)
+{
+    static std::mutex mu;
+    static cudaStream_t cache[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return fail(VEDA_ERR_CUDA, "no CUDA device");
+    std::lock_guard<std::mutex> lock(mu);
+    if (!cache[dev] && cudaStreamCreateWithFlags(&cache[dev], cudaStreamNonBlocking) != cudaSuccess)
+        return fail(VEDA_ERR_CUDA, "tile_select_pooled: stream creation failed");
+    *out = cache[dev];
     return VEDA_OK;
 }
 
@@ -435,7 +455,6 @@ veda_status veda_tile_select_pooled(const float *zq, const float *zk, const int3
     double *eq = reinterpret_cast<double *>(p); p += align256(rows * w->d_lat * sizeof(double));
     double *ek = reinterpret_cast<double *>(p); p += align256(rows * w->d_lat * sizeof(double));
     void *oz_scratch = p;
-    float *s_chunk = reinterpret_cast<float *>(static_cast<char *>(workspace) + score_ws);
     const float *wq[4] = {w->w1q, w->b1q, w->w2q, w->b2q}, *wk[4] = {w->w1k, w->b1k, w->w2k, w->b2k};
     if ((st = launch_ozaki_phi(zq, zk, Hh, n_tiles, w->d_in, w->d_hidden, w->d_lat, wq, wk, w->prepared, hid, eq, ek, oz_scratch,
                                S(stream))) != VEDA_OK)
@@ -444,19 +463,54 @@ veda_status veda_tile_select_pooled(const float *zq, const float *zk, const int3
         VEDA_OK)
         return st;
     const int hc = select_chunk_heads(Hh, n_tiles, heads_per_chunk);
-    for (int h0 = 0; h0 < Hh; h0 += hc) {
+    const int nbuf = select_buffers(Hh, hc);
+    const size_t buf_bytes = align256((size_t)hc * n_tiles * n_tiles * sizeof(float));
+    cudaStream_t ms = S(stream), side = ms;
+    if (nbuf == 2 && (st = select_side_stream(&side)) != VEDA_OK) return st;
+    std::vector<cudaEvent_t> ev;  // per chunk: scores written (main) / top-k done (side)
+    auto event = [&]() -> cudaEvent_t {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        ev.push_back(e);
+        return e;
+    };
+    cudaEvent_t last_topk = nullptr;
+    auto finish = [&](veda_status r) {
+        // the caller's stream resumes only after the last top-k (the side stream is in order);
+        // also on an error, so no side-stream work outlives the call unseen
+        if (side != ms && last_topk) cudaStreamWaitEvent(ms, last_topk, 0);
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);  // released once the device passes them
+        return r;
+    };
+    std::vector<cudaEvent_t> topk_done;
+    int c = 0;
+    for (int h0 = 0; h0 < Hh; h0 += hc, ++c) {
         const int hn = std::min(hc, Hh - h0);
+        float *s_chunk = reinterpret_cast<float *>(static_cast<char *>(workspace) + score_ws + (c % nbuf) * buf_bytes);
+        if (c >= nbuf && side != ms) cudaStreamWaitEvent(ms, topk_done[c - nbuf], 0);  // buffer read by top-k c-2
         if ((st = launch_ozaki_score_gemm(tile_count, Hh, h0, hn, n_tiles, w->d_in, w->d_hidden, w->d_lat, s_chunk,
-                                          oz_scratch, S(stream))) != VEDA_OK)
-            return st;
-        if (debug_mode() && (st = debug_validate(S(stream), [&](uint32_t *f) {
-                                 return launch_validate_scores(s_chunk, (int64_t)hn * n_tiles * n_tiles, f, S(stream));
+                                          oz_scratch, ms)) != VEDA_OK)
+            return finish(st);
+        if (debug_mode() && (st = debug_validate(ms, [&](uint32_t *f) {
+                                 return launch_validate_scores(s_chunk, (int64_t)hn * n_tiles * n_tiles, f, ms);
                              })) != VEDA_OK)
-            return st;
-        if ((st = launch_topk(s_chunk, hn, n_tiles, k, idx + (size_t)h0 * n_tiles * k, S(stream))) != VEDA_OK)
-            return st;
+            return finish(st);
+        if (side != ms) {
+            cudaEvent_t g = event();
+            if (!g || cudaEventRecord(g, ms) != cudaSuccess || cudaStreamWaitEvent(side, g, 0) != cudaSuccess)
+                return finish(fail(VEDA_ERR_CUDA, "tile_select_pooled: event record/wait failed"));
+        }
+        if ((st = launch_topk(s_chunk, hn, n_tiles, k, idx + (size_t)h0 * n_tiles * k, side)) != VEDA_OK)
+            return finish(st);
+        if (side != ms) {
+            cudaEvent_t t = event();
+            if (!t || cudaEventRecord(t, side) != cudaSuccess)
+                return finish(fail(VEDA_ERR_CUDA, "tile_select_pooled: event record failed"));
+            topk_done.push_back(t);
+            last_topk = t;
+        }
     }
-    return VEDA_OK;
+    return finish(VEDA_OK);
 }
 
 veda_status veda_select_topk(const float *scores, int32_t Hh, int32_t n_tiles, int32_t k, int32_t *idx, void *stream)
