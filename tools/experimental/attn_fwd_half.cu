@@ -1,0 +1,1083 @@
+// attn_fwd.cu -- tile-skipping FlashAttention forward for sm_100a (B200).
+//
+// Computes Eq. 2 of the paper: for every (head h, query tile i)
+//     O_i = softmax(Q~_i K^_i^T * scale) V^_i,   K^_i / V^_i = concat of the k kept tiles
+// visiting ONLY the kept key tiles named by idx[h][i][:] (producer
+// fetches "only the selected non-contiguous key/value tiles" into a circular buffer).
+//
+// B200 design:
+//  * persistent, one CTA per SM, 384 threads = 3 warpgroups:
+//      warp 0      TMA producer: Q tiles and the kept K/V tiles -> SMEM ring (SWIZZLE_128B)
+//      warp 1      MMA issuer (warp-uniform, one elected lane): tcgen05.mma,
+//                  S = Q K^T (SS) and O += P V (TS)
+//      warps 2-3   ring-stage release for slot 0 / slot 1 (warpgroup 0 gives its spare
+//                  registers to the softmax warpgroups with setmaxnreg)
+//      warps 4-11  two softmax warpgroups ("slots"), one query tile each, one row per thread
+//  * two addressing modes: tiled tensors [Hh][N_T][B][d] (2-D TMA boxes, tiled output), or
+//    TOK: tiles gathered from token order by one 5-D TMA box each and output rows stored
+//    straight to token order (no tiled copies; the path's mode)
+//  * each slot owns 256 TMEM columns: S (fp32, 128 cols; P aliases its first B/2 columns
+//    as packed bf16) and O (fp32, D cols).  The two slots work on different query
+//    tiles with independent kept lists, so one slot's softmax overlaps the other's MMAs.
+//  * online softmax in the log2 domain with lazy rescaling: O (in TMEM) is rescaled
+//    only when a row max grows by more than 8 (2^8 head-room in fp32/bf16).
+//  * padded key slots (slot_mask bit clear) get -inf; padded query rows are written 0.
+//  * ordering: the commit after S_{t} = Q K_t^T also covers the previous O += P_{t-1} V,
+//    so when softmax sees S_t, O is quiescent and may be rescaled in place.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+
+#include "attn_common.cuh"
+
+namespace veda {
+namespace attn {
+using namespace sm100;
+
+// A kept-tile list entry outside [0, n_tiles) (a caller bug; debug mode reports it as
+// VEDA_ERR_INDEX) is clamped, so the TMA coordinates and slot-mask reads stay inside the head.
+__device__ __forceinline__ int clamp_tile(int j, int NT) { return min(max(j, 0), NT - 1); }
+
+template <int B, int D>
+struct Geo {
+    static constexpr int QCHUNK = 128 * 128;         // one 64-col chunk of the 128-row Q buffer
+    static constexpr int Q_BYTES = QCHUNK * (D / 64);
+    static constexpr int KCHUNK = B * 128;           // one 64-col chunk of a B-row K/V tile
+    static constexpr int TILE_BYTES = KCHUNK * (D / 64);
+    static constexpr int NST_FIT = (VEDA_RING_BUDGET_KB * 1024 - NSLOT * Q_BYTES) / TILE_BYTES;
+    static constexpr int NST = NST_FIT > 8 ? 8 : NST_FIT;
+    static constexpr int MW = B / 32;
+    static constexpr int NPH = B / 64;                // P hand-off halves (64 keys each)
+    static constexpr int NBAR = 2 * NST + (4 + NPH) * NSLOT;
+    static constexpr int SMEM = NSLOT * Q_BYTES + NST * TILE_BYTES + NBAR * 8 + 16 + 1024;
+    static_assert(NST >= 2, "ring too shallow");
+};
+
+template <int B, int D, bool TOK>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
+                           const __grid_constant__ CUtensorMap tmK,
+                           const __grid_constant__ CUtensorMap tmV, const Params p,
+                           const __grid_constant__ TokParams tp)
+{
+    using G = Geo<B, D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                ~uintptr_t(1023));
+    const uint32_t sQ = smem_u32(smem);
+    const uint32_t sRing = sQ + NSLOT * G::Q_BYTES;
+    const uint32_t sBar = sRing + G::NST * G::TILE_BYTES;
+    uint32_t *tmem_slot =
+        reinterpret_cast<uint32_t *>(smem + NSLOT * G::Q_BYTES + G::NST * G::TILE_BYTES + G::NBAR * 8);
+    // barrier addresses
+#define RING_FULL(i) (sBar + 8u * (i))
+#define RING_EMPTY(i) (sBar + 8u * (G::NST + (i)))
+#define Q_FULL(s) (sBar + 8u * (2 * G::NST + (s)))
+#define Q_EMPTY(s) (sBar + 8u * (2 * G::NST + NSLOT + (s)))
+#define S_FULL(s) (sBar + 8u * (2 * G::NST + 2 * NSLOT + (s)))
+#define O_FULL(s) (sBar + 8u * (2 * G::NST + 3 * NSLOT + (s)))
+#define P_FULL(s, hf) (sBar + 8u * (2 * G::NST + (4 + (hf)) * NSLOT + (s)))
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (B < 128) {  // rows B..127 of the M=128 Q operand are never loaded: keep them zero
+        uint4 *q4 = reinterpret_cast<uint4 *>(smem);
+        for (int i = threadIdx.x; i < NSLOT * G::Q_BYTES / 16; i += NTHREADS) q4[i] = make_uint4(0, 0, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < G::NST; ++i) {
+            mbar_init(RING_FULL(i), 1);
+            mbar_init(RING_EMPTY(i), 1);
+        }
+        for (int s = 0; s < NSLOT; ++s) {
+            mbar_init(Q_FULL(s), 1);
+            mbar_init(Q_EMPTY(s), 1);
+            mbar_init(S_FULL(s), 1);
+            for (int hf = 0; hf < G::NPH; ++hf) mbar_init(P_FULL(s, hf), 128);
+            mbar_init(O_FULL(s), 1);
+        }
+        fence_barrier_init();
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+    }
+    if (warp == 1) {
+        tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+
+    const int NT = p.NT, K = p.k, total = p.unit0 + p.total_units;  // units end
+    const int gslots = gridDim.x * NSLOT;
+    const int rounds = (p.total_units + gslots - 1) / gslots;
+    // unit u = h*NT + i; consecutive CTAs/slots take consecutive query tiles of one head (L2 reuse)
+#define UNIT_OF(r, s) (p.unit0 + (r) * gslots + blockIdx.x * NSLOT + (s))
+
+    if (warp < 4) {
+#ifndef VEDA_NO_SETMAXNREG
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS_CTRL));
+#endif
+    if (lane == 0) DBG("w%d ctrl start tbase=%x\n", warp, tbase);
+    if (warp == 0) {
+        // ============================ TMA producer ============================
+        if (lane == 0) {
+            uint32_t stage = 0, ph = 0;
+            uint32_t qe_bits = 0;  // per-slot phase bits of Q_EMPTY
+            for (int r = 0; r < rounds; ++r) {
+                int u[NSLOT], hh[NSLOT], jv[NSLOT];
+                bool act[NSLOT];
+                const int32_t *il[NSLOT];
+#pragma unroll
+                for (int s = 0; s < NSLOT; ++s) {
+                    u[s] = UNIT_OF(r, s);
+                    act[s] = u[s] < total;
+                    hh[s] = act[s] ? u[s] / NT : 0;
+                    il[s] = p.idx + (size_t)(act[s] ? u[s] : 0) * K;
+                }
+#pragma unroll
+                for (int s = 0; s < NSLOT; ++s) {
+                    if (!act[s]) continue;
+                    mbar_wait(Q_EMPTY(s), ((qe_bits >> s) & 1u) ^ 1u);
+                    qe_bits ^= 1u << s;
+                    mbar_expect_tx(Q_FULL(s), B * D * 2);
+#pragma unroll
+                    if (TOK)
+                        tma_tile_tok<D / 64>(sQ + s * G::Q_BYTES, G::QCHUNK, tp.q, tp, hh[s], u[s] - hh[s] * NT,
+                                             Q_FULL(s));
+                    else
+                        for (int c = 0; c < D / 64; ++c)
+                            tma_load_2d(sQ + s * G::Q_BYTES + c * G::QCHUNK, &tmQ, c * 64, u[s] * B, Q_FULL(s));
+                }
+                auto load_tile = [&](const CUtensorMap *tm, int h, int j) {
+                    mbar_wait(RING_EMPTY(stage), ph ^ 1);
+#ifdef VEDA_DBG_SKIP_V  // timing experiment only: V tiles are not loaded (wrong results)
+                    if (tm == &tmV) {
+                        mbar_expect_tx(RING_FULL(stage), 0);
+                        if (++stage == G::NST) { stage = 0; ph ^= 1; }
+                        return;
+                    }
+#endif
+                    mbar_expect_tx(RING_FULL(stage), G::TILE_BYTES);
+                    const int row = (h * NT + j) * B;
+                    if (TOK)
+                        tma_tile_tok<D / 64>(sRing + stage * G::TILE_BYTES, G::KCHUNK, tm == &tmK ? tp.k : tp.v, tp,
+                                             h, j, RING_FULL(stage));
+                    else
+#pragma unroll
+                        for (int c = 0; c < D / 64; ++c)
+                            tma_load_2d(sRing + stage * G::TILE_BYTES + c * G::KCHUNK, tm, c * 64, row,
+                                        RING_FULL(stage));
+                    if (++stage == G::NST) { stage = 0; ph ^= 1; }
+                };
+#pragma unroll
+                for (int s = 0; s < NSLOT; ++s)
+                    if (act[s]) { jv[s] = clamp_tile(__ldg(il[s]), NT); load_tile(&tmK, hh[s], jv[s]); }
+                for (int t = 0; t < K; ++t) {
+#pragma unroll
+                    for (int s = 0; s < NSLOT; ++s) {
+                        if (!act[s]) continue;
+                        const int jn = (t + 1 < K) ? clamp_tile(__ldg(il[s] + t + 1), NT) : 0;
+                        load_tile(&tmV, hh[s], jv[s]);
+                        if (t + 1 < K) { jv[s] = jn; load_tile(&tmK, hh[s], jv[s]); }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 2 || warp == 3) {
+        // ============================ ring-stage release ============================
+        // Warp 2 (slot 0) / warp 3 (slot 1): S_FULL(s) of tile t lands only when QK(s,t)
+        // and every earlier MMA of the issuing thread -- in particular PV(s,t-1) -- are
+        // complete, so the stages of K(s,t) and V(s,t-1) can go back to the producer at
+        // once (O_FULL releases the unit's last V).  Keeping this off the MMA thread and
+        // off the softmax keeps stage hold times short with a 5-stage ring.
+        if (lane == 0) {
+            const int s = warp - 2;
+            uint32_t sf_ph = 0, of_ph = 0;
+            for (int r = 0; r < rounds; ++r) {
+                if (UNIT_OF(r, s) >= total) break;
+                const int A = (UNIT_OF(r, 1) < total) ? 2 : 1;
+                const uint32_t base = (uint32_t)r * (2 * NSLOT) * (uint32_t)K;
+                // global load index of K(s,t) / V(s,t) in the producer's order
+                auto gk = [&](int t) -> uint32_t { return base + (t == 0 ? s : A + 2 * A * (t - 1) + 2 * s + 1); };
+                auto gv = [&](int t) -> uint32_t { return base + A + 2 * A * t + ((t < K - 1) ? 2 * s : s); };
+                for (int t = 0; t < K; ++t) {
+                    mbar_wait(S_FULL(s), sf_ph);
+                    sf_ph ^= 1;
+                    mbar_arrive(RING_EMPTY(gk(t) % G::NST));
+                    if (t > 0) mbar_arrive(RING_EMPTY(gv(t - 1) % G::NST));
+                }
+                mbar_wait(O_FULL(s), of_ph);
+                of_ph ^= 1;
+                mbar_arrive(RING_EMPTY(gv(K - 1) % G::NST));
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ============================ MMA issuer ============================
+        // One thread issues, slot by slot, groups [PV(s,t) ; QK(s,t+1)] back to back (the
+        // QK reuses the S/P columns, so it must follow the PV: same thread => in order).
+        // Before a group, the three barriers it needs (P(s,t), the V stage, the next K
+        // stage) are probed in ONE asm block so their latencies overlap; only a barrier
+        // that is not yet complete is then waited on.  Ring stages are released by the
+        // softmax warps; the MMA thread only commits S_FULL (+ Q_EMPTY / O_FULL).
+        // The whole warp runs the loop (warp-uniform values, one lane issues via elect.sync:
+        // see sm100.cuh mma_ss_w); descriptors are advanced by constant offsets.
+        {
+            constexpr uint32_t idesc_qk = idesc_bf16_f32(128, B, 0, 0);  // Q, K both K-major
+            constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D, 0, 1);  // P K-major (TMEM), V MN-major
+            uint32_t stage = 0, ph = 0;
+            uint32_t qf_bits = 0, pf_bits = 0;  // per-slot phase bits of Q_FULL / P_FULL
+            int nqk = 0, npv = 0;
+            (void)nqk; (void)npv;
+            auto next_stage = [&](uint32_t &st, uint32_t &sp) {
+                st = stage;
+                sp = ph;
+                if (++stage == G::NST) { stage = 0; ph ^= 1; }
+            };
+            auto issue_qk = [&](int s, int t, uint32_t st) {
+                const uint64_t ad0 = sdesc_sw128(sQ + s * G::Q_BYTES, 16, 1024);
+                const uint64_t bd0 = sdesc_sw128(sRing + st * G::TILE_BYTES, 16, 1024);
+                const uint32_t tS = tbase + s * 256;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint64_t ao = (uint64_t)(((kk >> 2) * G::QCHUNK + (kk & 3) * 32) >> 4);
+                    const uint64_t bo = (uint64_t)(((kk >> 2) * G::KCHUNK + (kk & 3) * 32) >> 4);
+                    mma_ss_w(tS, ad0 + ao, bd0 + bo, idesc_qk, kk > 0 ? 1u : 0u);
+                }
+                tc_commit_w(S_FULL(s));
+                if (t == K - 1) tc_commit_w(Q_EMPTY(s));
+            };
+            auto issue_pv = [&](int s, int t, uint32_t st, int hf) {
+                // V tile as the MN-major B operand: 16 keys = 16 rows of 128 B; the second
+                // 64-wide chunk of d sits one KCHUNK further (LBO).  Half hf = keys
+                // [64 hf, 64 hf + 64), i.e. the P columns of hand-off hf.
+                const uint64_t vd0 = sdesc_sw128(sRing + st * G::TILE_BYTES, G::KCHUNK, 1024);
+                const uint32_t tP = tbase + s * 256, tO = tbase + s * 256 + 128;
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4) {
+                    const int kk = hf * 4 + k4;
+                    mma_ts_w(tO, tP + kk * 8, vd0 + (uint64_t)((kk * 2048) >> 4), idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
+                }
+                if (t == K - 1 && hf == G::NPH - 1) tc_commit_w(O_FULL(s));
+            };
+            for (int r = 0; r < rounds; ++r) {
+                uint32_t act_bits = 0;
+#pragma unroll
+                for (int s = 0; s < NSLOT; ++s) act_bits |= (UNIT_OF(r, s) < total ? 1u : 0u) << s;
+                for (int s = 0; s < NSLOT; ++s) {
+                    if (!((act_bits >> s) & 1u)) continue;
+                    uint32_t st, sp;
+                    next_stage(st, sp);
+                    mbar_wait(Q_FULL(s), (qf_bits >> s) & 1u);
+                    qf_bits ^= 1u << s;
+                    mbar_wait(RING_FULL(st), sp);
+                    TR(0, nqk, 0);
+                    tc_fence_after();
+                    issue_qk(s, 0, st);
+                    TR(0, nqk, 2);
+                    ++nqk;
+                }
+                for (int t = 0; t < K; ++t) {
+                    for (int s = 0; s < NSLOT; ++s) {
+                        if (!((act_bits >> s) & 1u)) continue;
+                        const bool more = t + 1 < K;
+                        uint32_t sv, vp, sk = 0, kp = 0;
+                        next_stage(sv, vp);
+                        if (more) next_stage(sk, kp);
+                        const uint32_t pp = (pf_bits >> s) & 1u;
+                        pf_bits ^= 1u << s;
+                        TR(0, npv, 3);
+                        // non-blocking probe of the group's barriers (test_wait: an incomplete
+                        // P_FULL must not put the thread to sleep), then wait for the rest
+                        const uint32_t ok = mbar_try_wait4(P_FULL(s, 0), pp, RING_FULL(sv), vp,
+                                                           RING_FULL(more ? sk : sv), more ? kp : vp,
+                                                           RING_FULL(sv), vp);
+                        if (!(ok & 1u)) mbar_wait(P_FULL(s, 0), pp);
+                        if (!(ok & 2u)) mbar_wait(RING_FULL(sv), vp);
+                        if (more && !(ok & 4u)) mbar_wait(RING_FULL(sk), kp);
+                        TR(0, npv, 4);
+                        tc_fence_after();
+                        // P arrives in two halves: the first half's PV runs while the softmax
+                        // still exponentiates the second (shortens the S -> P -> S chain per slot)
+                        issue_pv(s, t, sv, 0);
+                        if (G::NPH == 2) {
+                            mbar_wait(P_FULL(s, 1), pp);
+                            TR(0, npv, 6);
+                            tc_fence_after();
+                            issue_pv(s, t, sv, 1);
+                        }
+                        if (more) issue_qk(s, t + 1, sk);
+                        TR(0, npv, 5);
+                        ++npv;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    } else {
+#ifndef VEDA_NO_SETMAXNREG
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_SOFTMAX));
+#endif
+        if (lane == 0) DBG("w%d softmax start\n", warp);
+        // ============================ softmax warpgroups ============================
+        const int slot = (warp - 4) >> 2;
+        const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+        const uint32_t tS = tbase + lane_off + slot * 256;
+        const uint32_t tO = tS + 128;
+        const float sl2 = p.scale_log2;
+        uint32_t sf_ph = 0, of_ph = 0;
+        for (int r = 0; r < rounds; ++r) {
+            const int u = UNIT_OF(r, slot);
+            if (u >= total) break;
+            const int h = u / NT;
+            const int32_t *il = p.idx + (size_t)u * K;
+            const uint32_t *mbase = p.slot_mask + (size_t)h * NT * G::MW;
+            float m = -INFINITY, l = 0.f;
+            int jn = clamp_tile(__ldg(il), NT);
+            for (int t = 0; t < K; ++t) {
+                uint32_t mk[G::MW];
+#pragma unroll
+                for (int w = 0; w < G::MW; ++w) mk[w] = __ldg(mbase + (size_t)jn * G::MW + w);
+                if (t + 1 < K) jn = clamp_tile(__ldg(il + t + 1), NT);
+
+                const int trs = r * K + t, trr = 1 + slot * 4 + quarter;  // trace role per softmax warp
+                if (lane == 0) TR(trr, trs, 0);
+                mbar_wait(S_FULL(slot), sf_ph);
+                if (lane == 0) TR(trr, trs, 1);
+                sf_ph ^= 1;
+                if (lane == 0) DBG("w%d slot%d t%d S ok\n", warp, slot, t);
+                tc_fence_after();
+                uint32_t sr[B / 32][32];
+#pragma unroll
+                for (int c = 0; c < B / 32; ++c) tmem_ld32(tS + c * 32, sr[c]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < B / 32; ++c) reg_fence(sr[c]);
+                if (lane == 0) TR(trr, trs, 2);
+
+                bool full = true;
+#pragma unroll
+                for (int w = 0; w < G::MW; ++w) full &= (mk[w] == 0xFFFFFFFFu);
+                if (!full) {
+#pragma unroll
+                    for (int c = 0; c < B / 32; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (!((mk[c] >> i) & 1u)) sr[c][i] = f2u(-INFINITY);
+                }
+                // row max with 8 independent partial maxima (no 128-long dependency chain)
+                float pm[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pm[q] = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < B / 32; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2)  // three-input maxima (FMNMX3): half the instructions
+                        pm[(i >> 1) & 7] = fmax3f(pm[(i >> 1) & 7], u2f(sr[c][i]), u2f(sr[c][i + 1]));
+                const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                       fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+                const float mnew = fmaxf(m, mx * sl2);
+                if (lane == 0 && mnew != 1.2345f) TR(trr, trs, 3);
+                // lazy rescale: only when some row of this warp grew its max by > 8 (log2 units)
+                float f = 1.f;
+                bool rescale = false;
+                if (t == 0) {
+                    m = mnew;
+                } else if (__any_sync(0xFFFFFFFFu, mnew > m + 8.0f)) {
+                    f = (mnew == -INFINITY) ? 1.f : ex2(m - mnew);
+                    rescale = true;
+                    l *= f;
+                    m = mnew;
+                }
+                const float mu = (m == -INFINITY) ? 0.f : m;
+                float ps[4] = {0.f, 0.f, 0.f, 0.f};
+                // P is handed to the MMA thread in halves of 64 keys (P_FULL(slot, half)):
+                // P V of the first half runs while the second half is exponentiated
+#pragma unroll
+                for (int c2 = 0; c2 < B / 64; ++c2) {
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int c = 2 * c2 + (i >> 4), e = (i & 15) * 2;
+                        float x0, x1;
+                        ffma2_bc(x0, x1, u2f(sr[c][e]), u2f(sr[c][e + 1]), sl2, -mu);
+                        float a, b;
+                        if (EMU_EVERY > 0 && (i % EMU_EVERY) == EMU_EVERY - 1) {
+                            ex2_emu2(a, b, x0, x1);  // FMA-pipe polynomial: unloads the MUFU unit
+                        } else {
+                            a = ex2(x0);
+                            b = ex2(x1);
+                        }
+                        fadd2_acc(ps[(i & 1) * 2], ps[(i & 1) * 2 + 1], a, b);
+                        pk[i] = pack_bf16(a, b);
+                    }
+                    tmem_st32(tS + c2 * 32, pk);  // P (bf16 pairs) over S columns already read
+                    if (c2 == 0 && rescale) {  // O is quiescent (see header); scale it before PV_t accumulates
+#pragma unroll
+                        for (int c = 0; c < D / 32; ++c) {
+                            uint32_t o[32];
+                            tmem_ld32(tO + c * 32, o);
+                            tmem_wait_ld();
+                            reg_fence(o);
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * f);
+                            tmem_st32(tO + c * 32, o);
+                        }
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(P_FULL(slot, c2));
+                    if (lane == 0) TR(trr, trs, 4 + c2);
+                }
+                l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+                if (lane == 0 && rescale) TR(trr, trs, 6);
+                if (lane == 0) DBG("w%d slot%d t%d P arrive l=%f m=%f\n", warp, slot, t, l, m);
+            }
+            // ---- epilogue: O / l -> bf16, padded query rows -> 0
+            mbar_wait(O_FULL(slot), of_ph);
+            of_ph ^= 1;
+            tc_fence_after();
+            bool qvalid = false;
+            if (row < B) qvalid = (__ldg(p.slot_mask + (size_t)u * G::MW + (row >> 5)) >> (row & 31)) & 1u;
+            const float inv = (qvalid && l > 0.f) ? 1.f / l : 0.f;
+            uint16_t *orow = p.out + ((size_t)u * B + (row < B ? row : 0)) * D;
+            bool store = row < B;
+            if (TOK) {  // row -> its token (reading R3); padded query slots have none
+                const TileOrigin o = tile_origin(tp, h, u - h * NT);
+                const int lpw = __ffs(tp.pw[o.c]) - 1, lphw = lpw + __ffs(tp.ph[o.c]) - 1;
+                const int t = o.t0 + (row >> lphw), hq = o.h0 + ((row >> lpw) & (tp.ph[o.c] - 1)),
+                          w = o.w0 + (row & (tp.pw[o.c] - 1));
+                store = store && qvalid;
+                orow = p.out + (size_t)h * tp.o_hs + (((size_t)t * tp.H + hq) * tp.W + w) * tp.o_ts;
+            }
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                uint32_t o[32];
+                tmem_ld32(tO + c * 32, o);
+                tmem_wait_ld();
+                reg_fence(o);
+                if (store) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(u2f(o[2 * i]) * inv, u2f(o[2 * i + 1]) * inv);
+                    uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+                }
+            }
+            if (p.lse != nullptr && row < B)
+                p.lse[(size_t)u * B + row] = (qvalid && l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+        }
+    }
+#undef UNIT_OF
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tbase, TMEM_COLS);
+    }
+}
+
+// ==========================================================================================
+// Half-tile schedule (B = 128): every kept tile is processed as two 64-key blocks.  Per slot
+// the TMEM holds S of BOTH halves (S0 | S1, 64 columns each; P_h packed over the first 32
+// columns of S_h) and O (D columns): 2 x (64 + 64 + 128) = 512.  The MMA warp issues, per
+// slot and tile, [PV_0(t) ; QK_0(t+1)] once P_0(t) is in and [PV_1(t) ; QK_1(t+1)] once
+// P_1(t) is in, so while the softmax works on one half the other half's PV and next QK run:
+// the softmax never waits for the tensor core's [PV ; QK] of the block it just handed over.
+// QK of a half is an N = 64 SS MMA (48 clk against 32 nominal: bound by the 128 B/clk
+// shared-memory operand read), so one tile costs ~1240 clk of tensor time instead of 1024;
+// the gain is that the chain S -> softmax -> P -> [PV ; QK] -> S no longer serialises.
+// Lazy rescaling: O may only be scaled when the PV of the previous block has finished,
+// which the softmax waits for (PV_DONE) only in the rare rescale case.
+template <int D, bool TOK>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    sparse_attn_half_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                            const __grid_constant__ CUtensorMap tmV, const Params p,
+                            const __grid_constant__ TokParams tp)
+{
+    constexpr int B = 128, HB = 64;
+    using G = Geo<B, D>;
+    constexpr int NBARH = 2 * G::NST + 9 * NSLOT;  // ring + Q_FULL/EMPTY, S_FULL x2, P_FULL x2, PV_DONE x2, O_FULL
+    static_assert(NSLOT * G::Q_BYTES + G::NST * G::TILE_BYTES + NBARH * 8 + 16 + 1024 <= 232448, "shared memory");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                ~uintptr_t(1023));
+    const uint32_t sQ = smem_u32(smem);
+    const uint32_t sRing = sQ + NSLOT * G::Q_BYTES;
+    const uint32_t sBar = sRing + G::NST * G::TILE_BYTES;
+    uint32_t *tmem_slot =
+        reinterpret_cast<uint32_t *>(smem + NSLOT * G::Q_BYTES + G::NST * G::TILE_BYTES + NBARH * 8);
+#define H_RING_FULL(i) (sBar + 8u * (i))
+#define H_RING_EMPTY(i) (sBar + 8u * (G::NST + (i)))
+#define H_Q_FULL(s) (sBar + 8u * (2 * G::NST + (s)))
+#define H_Q_EMPTY(s) (sBar + 8u * (2 * G::NST + NSLOT + (s)))
+#define H_O_FULL(s) (sBar + 8u * (2 * G::NST + 2 * NSLOT + (s)))
+#define H_S_FULL(s, h) (sBar + 8u * (2 * G::NST + (3 + (h)) * NSLOT + (s)))
+#define H_P_FULL(s, h) (sBar + 8u * (2 * G::NST + (5 + (h)) * NSLOT + (s)))
+#define H_PV_DONE(s, h) (sBar + 8u * (2 * G::NST + (7 + (h)) * NSLOT + (s)))
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < G::NST; ++i) {
+            mbar_init(H_RING_FULL(i), 1);
+            mbar_init(H_RING_EMPTY(i), 1);
+        }
+        for (int s = 0; s < NSLOT; ++s) {
+            mbar_init(H_Q_FULL(s), 1);
+            mbar_init(H_Q_EMPTY(s), 1);
+            mbar_init(H_O_FULL(s), 1);
+            for (int h = 0; h < 2; ++h) {
+                mbar_init(H_S_FULL(s, h), 1);
+                mbar_init(H_P_FULL(s, h), 128);
+                mbar_init(H_PV_DONE(s, h), 1);
+            }
+        }
+        fence_barrier_init();
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+    }
+    if (warp == 1) {
+        tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+
+    const int NT = p.NT, K = p.k, total = p.unit0 + p.total_units;
+    const int gslots = gridDim.x * NSLOT;
+    const int rounds = (p.total_units + gslots - 1) / gslots;
+#define H_UNIT_OF(r, s) (p.unit0 + (r) * gslots + blockIdx.x * NSLOT + (s))
+
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS_CTRL));
+        if (warp == 0) {
+            // ======================= TMA producer (same order as the full-tile kernel)
+            if (lane == 0) {
+                uint32_t stage = 0, ph = 0, qe_bits = 0;
+                for (int r = 0; r < rounds; ++r) {
+                    int u[NSLOT], hh[NSLOT], jv[NSLOT];
+                    bool act[NSLOT];
+                    const int32_t *il[NSLOT];
+#pragma unroll
+                    for (int s = 0; s < NSLOT; ++s) {
+                        u[s] = H_UNIT_OF(r, s);
+                        act[s] = u[s] < total;
+                        hh[s] = act[s] ? u[s] / NT : 0;
+                        il[s] = p.idx + (size_t)(act[s] ? u[s] : 0) * K;
+                    }
+#pragma unroll
+                    for (int s = 0; s < NSLOT; ++s) {
+                        if (!act[s]) continue;
+                        mbar_wait(H_Q_EMPTY(s), ((qe_bits >> s) & 1u) ^ 1u);
+                        qe_bits ^= 1u << s;
+                        mbar_expect_tx(H_Q_FULL(s), B * D * 2);
+                        if (TOK)
+                            tma_tile_tok<D / 64>(sQ + s * G::Q_BYTES, G::QCHUNK, tp.q, tp, hh[s], u[s] - hh[s] * NT,
+                                                 H_Q_FULL(s));
+                        else
+#pragma unroll
+                            for (int c = 0; c < D / 64; ++c)
+                                tma_load_2d(sQ + s * G::Q_BYTES + c * G::QCHUNK, &tmQ, c * 64, u[s] * B, H_Q_FULL(s));
+                    }
+                    auto load_tile = [&](const CUtensorMap *tm, int h, int j) {
+                        mbar_wait(H_RING_EMPTY(stage), ph ^ 1);
+                        mbar_expect_tx(H_RING_FULL(stage), G::TILE_BYTES);
+                        const int row = (h * NT + j) * B;
+                        if (TOK)
+                            tma_tile_tok<D / 64>(sRing + stage * G::TILE_BYTES, G::KCHUNK, tm == &tmK ? tp.k : tp.v,
+                                                 tp, h, j, H_RING_FULL(stage));
+                        else
+#pragma unroll
+                            for (int c = 0; c < D / 64; ++c)
+                                tma_load_2d(sRing + stage * G::TILE_BYTES + c * G::KCHUNK, tm, c * 64, row,
+                                            H_RING_FULL(stage));
+                        if (++stage == G::NST) { stage = 0; ph ^= 1; }
+                    };
+#pragma unroll
+                    for (int s = 0; s < NSLOT; ++s)
+                        if (act[s]) { jv[s] = clamp_tile(__ldg(il[s]), NT); load_tile(&tmK, hh[s], jv[s]); }
+                    for (int t = 0; t < K; ++t) {
+#pragma unroll
+                        for (int s = 0; s < NSLOT; ++s) {
+                            if (!act[s]) continue;
+                            const int jn = (t + 1 < K) ? clamp_tile(__ldg(il[s] + t + 1), NT) : 0;
+                            load_tile(&tmV, hh[s], jv[s]);
+                            if (t + 1 < K) { jv[s] = jn; load_tile(&tmK, hh[s], jv[s]); }
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        } else if (warp == 2 || warp == 3) {
+            // ======================= ring-stage release: S_FULL of a tile's SECOND half implies
+            // both QKs of K(s,t) and (issue order) PV_1(s,t-1) are complete
+            if (lane == 0) {
+                const int s = warp - 2;
+                uint32_t sf_ph = 0, of_ph = 0;
+                for (int r = 0; r < rounds; ++r) {
+                    if (H_UNIT_OF(r, s) >= total) break;
+                    const int A = (H_UNIT_OF(r, 1) < total) ? 2 : 1;
+                    const uint32_t base = (uint32_t)r * (2 * NSLOT) * (uint32_t)K;
+                    auto gk = [&](int t) -> uint32_t { return base + (t == 0 ? s : A + 2 * A * (t - 1) + 2 * s + 1); };
+                    auto gv = [&](int t) -> uint32_t { return base + A + 2 * A * t + ((t < K - 1) ? 2 * s : s); };
+                    for (int t = 0; t < K; ++t) {
+                        mbar_wait(H_S_FULL(s, 1), sf_ph);
+                        sf_ph ^= 1;
+                        mbar_arrive(H_RING_EMPTY(gk(t) % G::NST));
+                        if (t > 0) mbar_arrive(H_RING_EMPTY(gv(t - 1) % G::NST));
+                    }
+                    mbar_wait(H_O_FULL(s), of_ph);
+                    of_ph ^= 1;
+                    mbar_arrive(H_RING_EMPTY(gv(K - 1) % G::NST));
+                }
+            }
+            __syncwarp();
+        } else if (warp == 1) {
+            // ======================= MMA warp
+            constexpr uint32_t idesc_qk = idesc_bf16_f32(128, HB, 0, 0);  // N = 64 keys
+            constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D, 0, 1);
+            uint32_t stage = 0, ph = 0, qf_bits = 0, pf_bits = 0;
+            auto next_stage = [&](uint32_t &st, uint32_t &sp) {
+                st = stage;
+                sp = ph;
+                if (++stage == G::NST) { stage = 0; ph ^= 1; }
+            };
+            // QK of half h of the K tile in stage st into S_h of slot s
+            auto issue_qk = [&](int s, int h, uint32_t st) {
+                const uint64_t ad0 = sdesc_sw128(sQ + s * G::Q_BYTES, 16, 1024);
+                const uint64_t bd0 = sdesc_sw128(sRing + st * G::TILE_BYTES + h * (HB * 128), 16, 1024);
+                const uint32_t tS = tbase + s * 256 + h * HB;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint64_t ao = (uint64_t)(((kk >> 2) * G::QCHUNK + (kk & 3) * 32) >> 4);
+                    const uint64_t bo = (uint64_t)(((kk >> 2) * G::KCHUNK + (kk & 3) * 32) >> 4);
+                    mma_ss_w(tS, ad0 + ao, bd0 + bo, idesc_qk, kk > 0 ? 1u : 0u);
+                }
+                tc_commit_w(H_S_FULL(s, h));
+            };
+            // PV of half h: keys [64h, 64h + 64) of the V tile in stage st, P_h from TMEM
+            auto issue_pv = [&](int s, int h, int t, uint32_t st) {
+                const uint64_t vd0 = sdesc_sw128(sRing + st * G::TILE_BYTES, G::KCHUNK, 1024);
+                const uint32_t tP = tbase + s * 256 + h * HB, tO = tbase + s * 256 + 128;
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4) {
+                    const int kk = h * 4 + k4;
+                    mma_ts_w(tO, tP + k4 * 8, vd0 + (uint64_t)((kk * 2048) >> 4), idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
+                }
+                tc_commit_w(H_PV_DONE(s, h));
+            };
+            for (int r = 0; r < rounds; ++r) {
+                uint32_t act_bits = 0;
+#pragma unroll
+                for (int s = 0; s < NSLOT; ++s) act_bits |= (H_UNIT_OF(r, s) < total ? 1u : 0u) << s;
+                for (int s = 0; s < NSLOT; ++s) {
+                    if (!((act_bits >> s) & 1u)) continue;
+                    uint32_t st, sp;
+                    next_stage(st, sp);
+                    mbar_wait(H_Q_FULL(s), (qf_bits >> s) & 1u);
+                    qf_bits ^= 1u << s;
+                    mbar_wait(H_RING_FULL(st), sp);
+                    tc_fence_after();
+                    issue_qk(s, 0, st);
+                    issue_qk(s, 1, st);
+                    if (K == 1) tc_commit_w(H_Q_EMPTY(s));
+                }
+                for (int t = 0; t < K; ++t) {
+                    const bool more = t + 1 < K;
+                    uint32_t sv[NSLOT], sk[NSLOT];
+                    for (int h = 0; h < 2; ++h) {
+                        for (int s = 0; s < NSLOT; ++s) {
+                            if (!((act_bits >> s) & 1u)) continue;
+                            const uint32_t pp = (pf_bits >> (2 * s + h)) & 1u;
+                            pf_bits ^= 1u << (2 * s + h);
+                            const int gn = (r * K + t) * 4 + h * 2 + s;
+                            TR(0, gn, 0);
+                            if (h == 0) {  // the tile's stages: V(s,t), K(s,t+1)
+                                uint32_t vp, kp = 0;
+                                next_stage(sv[s], vp);
+                                if (more) next_stage(sk[s], kp);
+                                const uint32_t ok = mbar_try_wait4(H_P_FULL(s, 0), pp, H_RING_FULL(sv[s]), vp,
+                                                                   H_RING_FULL(more ? sk[s] : sv[s]), more ? kp : vp,
+                                                                   H_RING_FULL(sv[s]), vp);
+                                if (!(ok & 1u)) mbar_wait(H_P_FULL(s, 0), pp);
+                                if (!(ok & 2u)) mbar_wait(H_RING_FULL(sv[s]), vp);
+                                if (more && !(ok & 4u)) mbar_wait(H_RING_FULL(sk[s]), kp);
+                            } else {
+                                mbar_wait(H_P_FULL(s, 1), pp);
+                            }
+                            TR(0, gn, 1);
+                            tc_fence_after();
+                            issue_pv(s, h, t, sv[s]);
+                            if (t == K - 1 && h == 1) tc_commit_w(H_O_FULL(s));
+                            if (more) {
+                                issue_qk(s, h, sk[s]);
+                                if (t + 1 == K - 1 && h == 1) tc_commit_w(H_Q_EMPTY(s));
+                            }
+                            TR(0, gn, 2);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_SOFTMAX));
+        // ======================= softmax warpgroups: blocks (t, 0), (t, 1), (t + 1, 0), ...
+        const int slot = (warp - 4) >> 2;
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+        const uint32_t tS0 = tbase + lane_off + slot * 256;
+        const uint32_t tO = tS0 + 128;
+        const float sl2 = p.scale_log2;
+        uint32_t sf_bits = 0, of_ph = 0;  // phases of S_FULL(h) (bit h), O_FULL
+        uint32_t nunits = 0;              // units this slot finished: PV_DONE(h) completed nunits*K times
+        for (int r = 0; r < rounds; ++r) {
+            const int u = H_UNIT_OF(r, slot);
+            if (u >= total) break;
+            const int h_ = u / NT;
+            const int32_t *il = p.idx + (size_t)u * K;
+            const uint32_t *mbase = p.slot_mask + (size_t)h_ * NT * G::MW;
+            float m = -INFINITY, l = 0.f;
+            int jn = clamp_tile(__ldg(il), NT);
+            uint32_t mk[G::MW];
+            for (int t = 0; t < K; ++t) {
+#pragma unroll
+                for (int w = 0; w < G::MW; ++w) mk[w] = __ldg(mbase + (size_t)jn * G::MW + w);
+                if (t + 1 < K) jn = clamp_tile(__ldg(il + t + 1), NT);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t tS = tS0 + h * HB;
+                    const int bn = (r * K + t) * 2 + h, trr = 1 + slot * 4 + quarter;
+                    (void)bn; (void)trr;
+                    if (lane == 0) TR(trr, bn, 0);
+                    mbar_wait(H_S_FULL(slot, h), (sf_bits >> h) & 1u);
+                    if (lane == 0) TR(trr, bn, 1);
+                    sf_bits ^= 1u << h;
+                    tc_fence_after();
+                    uint32_t sr[2][32];
+                    tmem_ld32(tS, sr[0]);
+                    tmem_ld32(tS + 32, sr[1]);
+                    tmem_wait_ld();
+                    reg_fence(sr[0]);
+                    reg_fence(sr[1]);
+                    const uint32_t mk0 = mk[2 * h], mk1 = mk[2 * h + 1];
+                    if ((mk0 & mk1) != 0xFFFFFFFFu) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            if (!((mk0 >> i) & 1u)) sr[0][i] = f2u(-INFINITY);
+                            if (!((mk1 >> i) & 1u)) sr[1][i] = f2u(-INFINITY);
+                        }
+                    }
+                    float pm[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) pm[q] = -INFINITY;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2)
+                            pm[(i >> 1) & 7] = fmax3f(pm[(i >> 1) & 7], u2f(sr[c][i]), u2f(sr[c][i + 1]));
+                    const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                           fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+                    const float mnew = fmaxf(m, mx * sl2);
+                    if (lane == 0 && mnew != 1.2345f) TR(trr, bn, 2);
+                    float f = 1.f;
+                    bool rescale = false;
+                    if (t == 0 && h == 0) {
+                        m = mnew;
+                    } else if (__any_sync(0xFFFFFFFFu, mnew > m + 8.0f)) {
+                        f = (mnew == -INFINITY) ? 1.f : ex2(m - mnew);
+                        rescale = true;
+                        l *= f;
+                        m = mnew;
+                    }
+                    const float mu = (m == -INFINITY) ? 0.f : m;
+                    float ps[4] = {0.f, 0.f, 0.f, 0.f};
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int c = i >> 4, e = (i & 15) * 2;
+                        float x0, x1;
+                        ffma2_bc(x0, x1, u2f(sr[c][e]), u2f(sr[c][e + 1]), sl2, -mu);
+                        const float a = ex2(x0), b = ex2(x1);
+                        fadd2_acc(ps[(i & 1) * 2], ps[(i & 1) * 2 + 1], a, b);
+                        pk[i] = pack_bf16(a, b);
+                    }
+                    tmem_st32(tS, pk);  // P_h (bf16 pairs of the 64 keys) over S_h's first 32 columns
+                    if (rescale) {
+                        // the previous block's PV (issued after this block's QK) may still run:
+                        // wait for it before scaling O (the block before (t,0) is (t-1,1))
+                        // predecessor block: (t-1, 1) for h = 0, (t, 0) for h = 1; its PV is
+                        // completion number nunits*K + t - 1 (resp. + t) of PV_DONE(h ^ 1), and the
+                        // one after it needs this warp's next P, so the parity wait cannot overshoot
+                        const uint32_t cidx = nunits * (uint32_t)K + (uint32_t)t - (h == 0 ? 1u : 0u);
+                        mbar_wait(H_PV_DONE(slot, h ^ 1), cidx & 1u);
+                        tc_fence_after();
+#pragma unroll
+                        for (int c = 0; c < D / 32; ++c) {
+                            uint32_t o[32];
+                            tmem_ld32(tO + c * 32, o);
+                            tmem_wait_ld();
+                            reg_fence(o);
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * f);
+                            tmem_st32(tO + c * 32, o);
+                        }
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(H_P_FULL(slot, h));
+                    if (lane == 0) TR(trr, bn, 3);
+                    l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+                }
+            }
+            // ---- epilogue
+            mbar_wait(H_O_FULL(slot), of_ph);
+            of_ph ^= 1;
+            tc_fence_after();
+            bool qvalid = false;
+            if (row < B) qvalid = (__ldg(p.slot_mask + (size_t)u * G::MW + (row >> 5)) >> (row & 31)) & 1u;
+            const float inv = (qvalid && l > 0.f) ? 1.f / l : 0.f;
+            uint16_t *orow = p.out + ((size_t)u * B + row) * D;
+            bool store = true;
+            if (TOK) {
+                const TileOrigin o = tile_origin(tp, h_, u - h_ * NT);
+                const int lpw = __ffs(tp.pw[o.c]) - 1, lphw = lpw + __ffs(tp.ph[o.c]) - 1;
+                const int t = o.t0 + (row >> lphw), hq = o.h0 + ((row >> lpw) & (tp.ph[o.c] - 1)),
+                          w = o.w0 + (row & (tp.pw[o.c] - 1));
+                store = qvalid;
+                orow = p.out + (size_t)h_ * tp.o_hs + (((size_t)t * tp.H + hq) * tp.W + w) * tp.o_ts;
+            }
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                uint32_t o[32];
+                tmem_ld32(tO + c * 32, o);
+                tmem_wait_ld();
+                reg_fence(o);
+                if (store) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(u2f(o[2 * i]) * inv, u2f(o[2 * i + 1]) * inv);
+                    uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+                }
+            }
+            if (p.lse != nullptr)
+                p.lse[(size_t)u * B + row] = (qvalid && l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+            ++nunits;
+        }
+    }
+#undef H_UNIT_OF
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tbase, TMEM_COLS);
+    }
+#undef H_RING_FULL
+#undef H_RING_EMPTY
+#undef H_Q_FULL
+#undef H_Q_EMPTY
+#undef H_O_FULL
+#undef H_S_FULL
+#undef H_P_FULL
+#undef H_PV_DONE
+}
+
+static unsigned long long *g_attn_trace = nullptr;
+
+#ifndef VEDA_ATTN_HALF
+#define VEDA_ATTN_HALF 1
+#endif
+
+template <int B, int D, bool TOK>
+static veda_status launch_kernel(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, const Params &p,
+                                 const TokParams &tp, int units, cudaStream_t stream)
+{
+    using G = Geo<B, D>;
+    int grid = (units + NSLOT - 1) / NSLOT;
+    const int nsm = num_sms();
+    if (grid > nsm) grid = nsm;
+    if constexpr (B == 128 && VEDA_ATTN_HALF) {
+        constexpr int SMEMH = NSLOT * G::Q_BYTES + G::NST * G::TILE_BYTES + (2 * G::NST + 9 * NSLOT) * 8 + 16 + 1024;
+        cudaError_t e = cudaFuncSetAttribute(sparse_attn_half_kernel<D, TOK>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMH);
+        if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        sparse_attn_half_kernel<D, TOK><<<grid, NTHREADS, SMEMH, stream>>>(mq, mk, mv, p, tp);
+    } else {
+        // set per launch: the attribute belongs to the current device's context
+        cudaError_t e = cudaFuncSetAttribute(sparse_attn_fwd_kernel<B, D, TOK>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        sparse_attn_fwd_kernel<B, D, TOK><<<grid, NTHREADS, G::SMEM, stream>>>(mq, mk, mv, p, tp);
+    }
+    count_launch();
+    return check_launch("sparse_attn_fwd");
+}
+
+static Params make_params(const int32_t *idx, const uint32_t *mask, uint16_t *o, float *lse, int Hh, int NT, int kk,
+                          float scale)
+{
+    Params p;
+    p.idx = idx;
+    p.slot_mask = mask;
+    p.out = o;
+    p.lse = lse;
+    p.NT = NT;
+    p.k = kk;
+    p.total_units = Hh * NT;
+    p.unit0 = 0;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    p.trace = g_attn_trace;
+    return p;
+}
+
+template <int B, int D>
+static veda_status launch(const uint16_t *q, const uint16_t *k, const uint16_t *v, const int32_t *idx,
+                          const uint32_t *mask, int Hh, int NT, int kk, float scale, uint16_t *o,
+                          float *lse, cudaStream_t stream)
+{
+    CUtensorMap mq, mk, mv;
+    const uint64_t rows = (uint64_t)Hh * NT * B;
+    veda_status st;
+    if ((st = make_tmap_bf16(&mq, q, rows, D, B)) != VEDA_OK) return st;
+    if ((st = make_tmap_bf16(&mk, k, rows, D, B)) != VEDA_OK) return st;
+    if ((st = make_tmap_bf16(&mv, v, rows, D, B)) != VEDA_OK) return st;
+    static TokParams tp_unused;  // zero-initialised; the tiled instantiation never reads it
+    return launch_kernel<B, D, false>(mq, mk, mv, make_params(idx, mask, o, lse, Hh, NT, kk, scale), tp_unused,
+                                      Hh * NT, stream);
+}
+
+// Token-layout launch: heads are split into consecutive groups with at most MAXC distinct
+// tile shapes; each group is one launch on pointers offset to its first head.
+template <int B, int D>
+static veda_status launch_tok(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t hs, int64_t ts,
+                              const HeadCfgs &cf, int Hh, int Hp, int Wp, int T, int H, int W, int NT,
+                              const int32_t *idx, const uint32_t *mask, int kk, float scale, uint16_t *o,
+                              int64_t o_hs, int64_t o_ts, float *lse, int u_begin, int u_end, cudaStream_t stream)
+{
+    TokParams tp{};  // host staging (3-4 KB, per call: thread-safe), passed by value to the kernel
+    CUtensorMap dummy;
+    memset(&dummy, 0, sizeof dummy);
+    const int MW = B / 32;
+    for (int h0 = 0; h0 < Hh;) {
+        int nc = 0, h1 = h0;
+        for (; h1 < Hh; ++h1) {
+            int c = 0;
+            while (c < nc && !(tp.pt[c] == cf.pt[h1] && tp.ph[c] == cf.ph[h1] && tp.pw[c] == cf.pw[h1])) ++c;
+            if (c == nc) {
+                if (nc == MAXC) break;
+                tp.pt[c] = cf.pt[h1]; tp.ph[c] = cf.ph[h1]; tp.pw[c] = cf.pw[h1];
+                ++nc;
+            }
+            tp.cid[h1 - h0] = (uint8_t)c;
+        }
+        const int hn = h1 - h0;
+        // units of this head group that fall in [u_begin, u_end) (flattened head x query tile)
+        const int g_lo = std::max(u_begin, h0 * NT), g_hi = std::min(u_end, h1 * NT);
+        if (g_lo >= g_hi) {
+            h0 = h1;
+            continue;
+        }
+        veda_status st;
+        int tm = 0;
+        for (int c = 0; c < nc; ++c) {
+            if ((st = make_tmap_tile_tokens(&tp.q[c], q + (size_t)h0 * hs, hs, ts, hn, T, H, W, D, tp.pt[c], tp.ph[c],
+                                            tp.pw[c], &tm)) != VEDA_OK ||
+                (st = make_tmap_tile_tokens(&tp.k[c], k + (size_t)h0 * hs, hs, ts, hn, T, H, W, D, tp.pt[c], tp.ph[c],
+                                            tp.pw[c], &tm)) != VEDA_OK ||
+                (st = make_tmap_tile_tokens(&tp.v[c], v + (size_t)h0 * hs, hs, ts, hn, T, H, W, D, tp.pt[c], tp.ph[c],
+                                            tp.pw[c], &tm)) != VEDA_OK)
+                return st;
+        }
+        for (int c = 0; c < nc; ++c) {
+            tp.nbw[c] = (uint32_t)(Wp / tp.pw[c]);
+            tp.nbhw[c] = (uint32_t)((Hp / tp.ph[c]) * (Wp / tp.pw[c]));
+            auto magic = [](uint32_t n) {  // ceil(2^32 / n), saturated for n = 1 (div_magic corrects by one)
+                const unsigned long long m = (0x100000000ull + n - 1) / n;
+                return (uint32_t)(m > 0xFFFFFFFFull ? 0xFFFFFFFFull : m);
+            };
+            tp.mbw[c] = magic(tp.nbw[c]);
+            tp.mbhw[c] = magic(tp.nbhw[c]);
+        }
+        tp.T = T; tp.H = H; tp.W = W; tp.Hp = Hp; tp.Wp = Wp;
+        tp.tok_major = tm;
+        tp.o_hs = o_hs;
+        tp.o_ts = o_ts;
+        Params p = make_params(idx + (size_t)h0 * NT * kk, mask + (size_t)h0 * NT * MW, o + (size_t)h0 * o_hs,
+                               lse ? lse + (size_t)h0 * NT * B : nullptr, hn, NT, kk, scale);
+        p.unit0 = g_lo - h0 * NT;
+        p.total_units = g_hi - g_lo;
+        if ((st = launch_kernel<B, D, true>(dummy, dummy, dummy, p, tp, p.total_units, stream)) != VEDA_OK) return st;
+        h0 = h1;
+    }
+    return VEDA_OK;
+}
+
+}  // namespace attn
+
+#ifdef VEDA_ATTN_TRACE
+extern "C" __attribute__((visibility("default"))) void veda_dbg_set_attn_trace(void *dev_buf)
+{
+    attn::g_attn_trace = static_cast<unsigned long long *>(dev_buf);
+}
+#endif
+
+veda_status launch_sparse_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                               const int32_t *idx, const uint32_t *mask, int Hh, int NT, int B, int d,
+                               int kk, float scale, uint16_t *o, float *lse, cudaStream_t s)
+{
+    if (B == 128 && d == 128) return attn::launch<128, 128>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
+    if (B == 128 && d == 64) return attn::launch<128, 64>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
+    if (B == 64 && d == 128) return attn::launch<64, 128>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
+    if (B == 64 && d == 64) return attn::launch<64, 64>(q, k, v, idx, mask, Hh, NT, kk, scale, o, lse, s);
+    return fail(VEDA_ERR_CONFIG, "sparse_attn_fwd: unsupported (B=%d, d=%d)", B, d);
+}
+
+veda_status launch_sparse_attn_tok(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t hs, int64_t ts,
+                                   const HeadCfgs &cf, int Hh, int Tp, int Hp, int Wp, int T, int H, int W, int B,
+                                   int NT, int d, const int32_t *idx, const uint32_t *mask, int kk, float scale,
+                                   uint16_t *o, int64_t o_hs, int64_t o_ts, float *lse, int u_begin, int u_end,
+                                   cudaStream_t s)
+{
+    (void)Tp;
+    // a stride that is never used (one token, or one head) may equal the other one; give it
+    // a distinct value so the 5-D tensor maps get a well-ordered dimension set
+    if (hs == ts) {
+        if ((int64_t)T * H * W == 1)
+            ts = hs * Hh;
+        else if (Hh == 1)
+            hs = ts * ((int64_t)T * H * W);
+        else
+            return fail(VEDA_ERR_ALIGN, "sparse_attn_fwd_tokens: head_stride == token_stride");
+    }
+#define VEDA_TOK_ARGS q, k, v, hs, ts, cf, Hh, Hp, Wp, T, H, W, NT, idx, mask, kk, scale, o, o_hs, o_ts, lse, u_begin, u_end, s
+    if (B == 128 && d == 128) return attn::launch_tok<128, 128>(VEDA_TOK_ARGS);
+    if (B == 128 && d == 64) return attn::launch_tok<128, 64>(VEDA_TOK_ARGS);
+    if (B == 64 && d == 128) return attn::launch_tok<64, 128>(VEDA_TOK_ARGS);
+    if (B == 64 && d == 64) return attn::launch_tok<64, 64>(VEDA_TOK_ARGS);
+#undef VEDA_TOK_ARGS
+    return fail(VEDA_ERR_CONFIG, "sparse_attn_fwd_tokens: unsupported (B=%d, d=%d)", B, d);
+}
+
+}  // namespace veda
+
+

@@ -80,6 +80,15 @@ __global__ void __launch_bounds__(256, 1) umma_rate(long long *clk, int reps, co
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
                     mma_ts_w(tO, tA + kk * 8, vd + (uint64_t)((kk * 2048) >> 4), id_pv, 1u);
+            } else if (MODE == 5) {  // half-tile group: [4 PV-TS (64 keys) ; 8 QK-SS N = 64]
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    mma_ts_w(tO, tA + kk * 8, vd + (uint64_t)((kk * 2048) >> 4), id_pv, 1u);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint64_t o = (uint64_t)(((kk >> 2) * CHUNK_Q + (kk & 3) * 32) >> 4);
+                    mma_ss_w(tS, qd + o, kd + o, id_qk64, kk > 0 ? 1u : 0u);
+                }
             }
         }
         tc_commit_w(smem_u32(&bar));
@@ -173,7 +182,7 @@ static double run(int grid, int reps, long long *d)
     cudaMemcpy(h, d, grid * sizeof(long long), cudaMemcpyDeviceToHost);
     double m = 0;
     for (int i = 0; i < grid; ++i) m += h[i];
-    const int per_rep = MODE == 4 ? 16 : 8;
+    const int per_rep = MODE == 4 ? 16 : (MODE == 5 ? 12 : 8);
     return m / grid / ((double)reps * per_rep);
 }
 
@@ -194,6 +203,11 @@ int main()
         c[3] = run<3>(grid, reps, d);
         c[4] = run<4>(grid, reps, d);
         for (int m = 0; m < 5; ++m) printf("grid %3d  %-40s %7.1f clk per MMA\n", grid, names[m], c[m]);
+    }
+    {
+        const double h0 = run<5, 0>(sms, reps, d), h2 = run<5, 2>(sms, reps, d), h5 = run<5, 5>(sms, reps, d);
+        printf("half-tile group [4 PV-TS ; 8 QK-SS N=64]: %.1f / %.1f / %.1f clk per MMA (alone / + tcgen05.ld+st / + bulk copies) = %.0f clk per group (nominal 4x64 + 8x32 = 512)\n",
+               h0, h2, h5, h0 * 12);
     }
     const char *intf[] = {"none", "tcgen05.ld x32 loop (4 warps)", "tcgen05.ld + st x32 loop", "st.shared 16 B loop", "ld.shared 16 B loop",
                           "bulk copies global->shared"};
