@@ -8,6 +8,10 @@
  *   veda_select_topk    exactly-k kept key tiles per row
  *   veda_sparse_attn_fwd tile-skipping attention
  *   veda_tile_unpermute  back to token order
+ * and the forms the token-layout path runs: veda_tile_pool_qk
+ * (tiling + TripPool of Q and K straight from token order, one launch),
+ * veda_tile_select_pooled (phi, S_pred and top-k per chunk of heads: no full score
+ * tensor), veda_sparse_attn_fwd_tokens (tiles gathered from / rows stored to token order).
  *
  * Conventions for every call
  *   - Pointers are DEVICE pointers unless marked "host".  bf16 tensors are passed
@@ -17,9 +21,12 @@
  *     no pointer after returning.  Host arrays are read during the call only.  The
  *     caller owns every buffer (workspace sizes come from the *_workspace helpers).
  *     Exceptions, all one-time or bounded: the first scoring call on a device uploads
- *     a 36 KB constant table (Phi for the GELU) into the library's static device
+ *     a 24 KB constant table (Phi for the GELU) into the library's static device
  *     memory and synchronises `stream` once; veda_sparse_attention_host creates two
- *     side streams per device on first use and a few events per call.
+ *     side streams per device on first use and a few events per call;
+ *     veda_tile_select_pooled with several head chunks runs its top-k on one library side
+ *     stream per device (created on first use, a few events per call) and makes `stream`
+ *     wait for it before returning control of the work to `stream`.
  *   - Errors are returned as veda_status; nothing is printed, thrown or aborted.
  *     Arguments (NULL pointers, shapes including empty ones, k range, alignment) are
  *     validated before the first device call, so they report the same status with or
@@ -41,7 +48,8 @@
  *   tiled tensor   [Hh][N_T][B][d] bf16, tile-contiguous (B*d*2 bytes per tile)
  *   tile_count     [Hh][N_T] int32  real tokens per tile
  *   slot_mask      [Hh][N_T][MW] uint32, bit b of a tile set iff slot b is real
- *   scores         [Hh][N_T][N_T] fp32
+ *   scores         [Hh][N_T][N_T] fp32 (the two-call and tiled forms; the path's fused
+ *                  select holds only a chunk of heads at a time)
  *   idx            [Hh][N_T][k] int32, kept key tiles of each query tile, ascending
  */
 #ifndef VEDA_H_
