@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 
@@ -582,11 +583,11 @@ veda_status gemm(const int8_t *As, const int8_t *Bs, int M, int N, int K, int ba
 // Taylor table of Phi for gelu_tab, uploaded once per device (static module memory)
 static veda_status phi_table_ready(cudaStream_t s)
 {
-    static bool done[64] = {false};
+    static std::atomic<bool> done[64];  // zero-initialised (static storage); set once per device
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) dev = 0;
-    if (done[dev]) return VEDA_OK;
+    if (done[dev].load(std::memory_order_acquire)) return VEDA_OK;
     static oz::PhiEntry tab[oz::PHI_N];
     const double inv_sqrt2pi = 0.39894228040143267794;
     for (int i = 0; i < oz::PHI_N; ++i) {
@@ -611,7 +612,7 @@ static veda_status phi_table_ready(cudaStream_t s)
     const cudaError_t e = cudaMemcpyToSymbolAsync(oz::g_phi_tab, tab, sizeof tab, 0, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "ozaki: Phi table upload: %s", cudaGetErrorString(e));
     if (cudaStreamSynchronize(s) != cudaSuccess) return fail(VEDA_ERR_CUDA, "ozaki: Phi table upload failed");
-    done[dev] = true;
+    done[dev].store(true, std::memory_order_release);  // a concurrent first call uploads the same bytes
     return VEDA_OK;
 }
 
