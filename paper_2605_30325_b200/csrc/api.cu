@@ -42,16 +42,17 @@ veda_status check_launch(const char *what)
 
 int num_sms()
 {
-    static int cache[64] = {0};
+    static std::atomic<int> cache[64];  // per device, zero until first queried
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) dev = 0;
-    if (cache[dev] == 0) {
-        int n = 0;
+    int n = cache[dev].load(std::memory_order_relaxed);
+    if (n == 0) {
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        cache[dev] = n > 0 ? n : 148;
+        if (n <= 0) n = 148;
+        cache[dev].store(n, std::memory_order_relaxed);
     }
-    return cache[dev];
+    return n;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
@@ -113,16 +114,16 @@ veda_status make_tmap_tile_tokens(CUtensorMap *map, const void *base, int64_t he
 
 veda_status check_arch()
 {
-    static int ok_dev = -1;
+    static std::atomic<unsigned long long> ok_devs{0};  // bit d: device d checked and sm_100
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return fail(VEDA_ERR_CUDA, "no CUDA device");
-    if (dev == ok_dev) return VEDA_OK;
+    if (dev >= 0 && dev < 64 && ((ok_devs.load(std::memory_order_relaxed) >> dev) & 1ull)) return VEDA_OK;
     int major = 0, minor = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
     if (major != 10 || minor != 0)
         return fail(VEDA_ERR_ARCH, "device %d is sm_%d%d; libveda is built for sm_100a", dev, major, minor);
-    ok_dev = dev;
+    if (dev >= 0 && dev < 64) ok_devs.fetch_or(1ull << dev, std::memory_order_relaxed);
     return VEDA_OK;
 }
 

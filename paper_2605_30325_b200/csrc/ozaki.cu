@@ -521,10 +521,13 @@ veda_status split_rows(const T *X, int R, int K, int64_t sr, int64_t sb, int bat
         const int nbx = (Rp + rpb - 1) / rpb, total = nbx * batch;
         dim3 grid(nbx, batch);
         if (GELU) {
-            static int per_sm = 0;  // per instantiation of split_rows<T, GELU>
-            if (per_sm == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess)
-                per_sm = 1;
-            if (per_sm < 1) per_sm = 1;
+            static std::atomic<int> cached{0};  // per instantiation of split_rows<T, GELU>
+            int per_sm = cached.load(std::memory_order_relaxed);
+            if (per_sm == 0) {
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess || per_sm < 1)
+                    per_sm = 1;
+                cached.store(per_sm, std::memory_order_relaxed);
+            }
             grid = dim3(std::min(total, per_sm * num_sms()), 1);
         }
         kern<<<grid, 256, 0, s>>>(X, R, K, sr, sb, Kp, batch, out, ex, img);
@@ -588,7 +591,7 @@ static veda_status phi_table_ready(cudaStream_t s)
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) dev = 0;
     if (done[dev].load(std::memory_order_acquire)) return VEDA_OK;
-    static oz::PhiEntry tab[oz::PHI_N];
+    oz::PhiEntry tab[oz::PHI_N];  // 24 KB host staging; the upload below is synchronised before return
     const double inv_sqrt2pi = 0.39894228040143267794;
     for (int i = 0; i < oz::PHI_N; ++i) {
         const double c = std::fma((double)i + 0.5, oz::PHI_W, -8.0);  // the device's centre, bit for bit
