@@ -774,3 +774,29 @@ def test_tile_pool_qk_equals_two_pools(V, name):
     for a, b in ((zq, zq1), (zk, zk1)):
         assert torch.equal(a.view(torch.int32), b.view(torch.int32))
     assert torch.equal(cnt, cnt1) and torch.equal(mask, mask1)
+
+
+def test_path_on_side_stream_and_nhd_layout(V):
+    """The token path run on a non-default stream (the fused select's side-stream events
+    must order against it) and on [N, Hh, d] token-major views gives the default-stream,
+    head-major output bit for bit, at a multi-chunk scorer configuration."""
+    from paper_2605_30325_b200 import synth
+
+    pre = synth.PRESETS["wan1.3b"]
+    dev = torch.device("cuda")
+    q, k, v = synth.qkv(pre, device=dev)
+    w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, random_bias=True).items()}
+    path = V.SparseAttention(pre.lat, [pre.cfg], pre.heads, pre.d, w, sparsity=pre.sparsity)
+    path.ws = V.SelectWorkspace(pre.heads, path.shape.n_tiles, pre.d, path.scorer, dev, heads_per_chunk=2)
+    o_ref = path(q, k, v).clone()
+    idx_ref = path.idx.clone()
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        o_side = path(q, k, v)
+    side.synchronize()
+    assert torch.equal(path.idx, idx_ref) and torch.equal(o_side.view(torch.int16), o_ref.view(torch.int16))
+    qn, kn, vn = (t.transpose(0, 1).contiguous() for t in (q, k, v))  # [N, Hh, d]
+    o_nhd = path(qn.transpose(0, 1), kn.transpose(0, 1), vn.transpose(0, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(path.idx, idx_ref) and torch.equal(o_nhd.view(torch.int16), o_ref.view(torch.int16))
