@@ -46,8 +46,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-chunk", type=int, default=0,
                     help="heads per chunk of the host pipeline (0 = library default, ceil(Hh/32))")
-    ap.add_argument("--cpu-sample-units", type=int, default=240,
-                    help="query tiles of one head the cpu_baseline times (240 = 1/8 of a Waver head)")
+    ap.add_argument("--cpu-sample-units", type=int, default=720,
+                    help="query tiles of one head the cpu_baseline times (720 = 3/8 of a Waver head: "
+                         "with the head's tiling and scoring, ~10 s of oracle work on 16 cores)")
     ap.add_argument("--ref-sample-units", type=int, default=48,
                     help="query tiles per step of the --impl reference arm (a different sample each step)")
     ap.add_argument("--ulysses-chunks", type=int, default=3,
