@@ -39,6 +39,14 @@ namespace veda {
 namespace attn {
 using namespace sm100;
 
+// 32 bytes (words w0 .. w0 + 7 of pk) to global memory in one 256-bit store
+__device__ __forceinline__ void st_global_v8(void *dst, const uint32_t (&pk)[16], int w0)
+{
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(pk[w0]), "r"(pk[w0 + 1]),
+                 "r"(pk[w0 + 2]), "r"(pk[w0 + 3]), "r"(pk[w0 + 4]), "r"(pk[w0 + 5]), "r"(pk[w0 + 6]), "r"(pk[w0 + 7])
+                 : "memory");
+}
+
 // A kept-tile list entry outside [0, n_tiles) (a caller bug; debug mode reports it as
 // VEDA_ERR_INDEX) is clamped, so the TMA coordinates and slot-mask reads stay inside the head.
 __device__ __forceinline__ int clamp_tile(int j, int NT) { return min(max(j, 0), NT - 1); }
@@ -446,13 +454,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (lane == 0 && rescale) TR(trr, trs, 6);
                 if (lane == 0) DBG("w%d slot%d t%d P arrive l=%f m=%f\n", warp, slot, t, l, m);
             }
-            // ---- epilogue: O / l -> bf16, padded query rows -> 0
-            mbar_wait(O_FULL(slot), of_ph);
-            of_ph ^= 1;
-            tc_fence_after();
+            // ---- epilogue: O / l -> bf16, padded query rows -> 0.  The row's destination and
+            // validity do not depend on O: computed (global load included) before the wait
             bool qvalid = false;
             if (row < B) qvalid = (__ldg(p.slot_mask + (size_t)u * G::MW + (row >> 5)) >> (row & 31)) & 1u;
-            const float inv = (qvalid && l > 0.f) ? 1.f / l : 0.f;
             uint16_t *orow = p.out + ((size_t)u * B + (row < B ? row : 0)) * D;
             bool store = row < B;
             if (TOK) {  // row -> its token (reading R3); padded query slots have none
@@ -463,19 +468,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 store = store && qvalid;
                 orow = p.out + (size_t)h * tp.o_hs + (((size_t)t * tp.H + hq) * tp.W + w) * tp.o_ts;
             }
+            const float inv = (qvalid && l > 0.f) ? 1.f / l : 0.f;
+            mbar_wait(O_FULL(slot), of_ph);
+            of_ph ^= 1;
+            tc_fence_after();
+            {
+                uint32_t o[D / 32][32];  // all of the row's O in flight at once, one wait
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                uint32_t o[32];
-                tmem_ld32(tO + c * 32, o);
+                for (int c = 0; c < D / 32; ++c) tmem_ld32(tO + c * 32, o[c]);
                 tmem_wait_ld();
-                reg_fence(o);
+#pragma unroll
+                for (int c = 0; c < D / 32; ++c) reg_fence(o[c]);
                 if (store) {
-                    uint32_t pk[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(u2f(o[2 * i]) * inv, u2f(o[2 * i + 1]) * inv);
-                    uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
+                    for (int c = 0; c < D / 32; ++c) {
+                        uint32_t pk[16];
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+                        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(u2f(o[c][2 * i]) * inv, u2f(o[c][2 * i + 1]) * inv);
+                        st_global_v8(orow + c * 32, pk, 0);   // 32-byte stores: whole sectors
+                        st_global_v8(orow + c * 32 + 16, pk, 8);
+                    }
                 }
             }
             if (p.lse != nullptr && row < B)

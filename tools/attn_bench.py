@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--regime", default="path")
     ap.add_argument("--workload", default="waver12b")
+    ap.add_argument("--sparsity", type=float, default=None, help="override the workload's sparsity")
     ap.add_argument("--tokens", action="store_true", help="time the token-layout kernel (the path's) instead")
     a = ap.parse_args()
     veda.load()
@@ -26,7 +27,7 @@ def main():
     heads = list(range(a.heads))
     q, k, v = synth.qkv(pre, heads=heads, device=dev)
     w = {n: t.to(dev) for n, t in synth.scorer_weights(pre, heads=heads).items()}
-    path = veda.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity, device=dev, mode="tiled")
+    path = veda.SparseAttention(pre.lat, [pre.cfg], len(heads), pre.d, w, sparsity=pre.sparsity if a.sparsity is None else a.sparsity, device=dev, mode="tiled")
     path(q, k, v)
     NT, B, kk = path.shape.n_tiles, path.shape.B, path.k
     if a.regime == "random":
@@ -53,7 +54,7 @@ def main():
     ms = e0.elapsed_time(e1) / a.reps
     flops = 4.0 * B * B * pre.d * kk * NT * len(heads)
     print(f"{os.environ.get('VEDA_LIB', 'libveda.so').split('/')[-1]:28s} {a.regime:6s} heads={a.heads} "
-          f"{'tokens' if a.tokens else 'tiled'} "
+          f"{'tokens' if a.tokens else 'tiled'} k={kk} "
           f"{ms:8.3f} ms  {flops / ms / 1e9:7.1f} TFLOP/s", flush=True)
     return out
 

@@ -18,10 +18,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--heads", type=int, default=2)
     ap.add_argument("--steps", type=int, default=24)
+    ap.add_argument("--sparsity", type=float, default=None)
     a = ap.parse_args()
     lib = veda.load()
     lib.veda_dbg_set_attn_trace.argtypes = [ctypes.c_void_p]
     pre = synth.PRESETS["waver12b"]
+    if a.sparsity is not None:
+        pre = synth.Preset(pre.name, pre.lat, pre.heads, pre.d, pre.cfg, a.sparsity)
     dev = torch.device("cuda")
     heads = list(range(a.heads))
     q, k, v = synth.qkv(pre, heads=heads, device=dev)
