@@ -140,62 +140,68 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) {
             uint32_t stage = 0, ph = 0;
             uint32_t qe_bits = 0;  // per-slot phase bits of Q_EMPTY
-            for (int r = 0; r < rounds; ++r) {
-                int u[NSLOT], hh[NSLOT], jv[NSLOT];
-                bool act[NSLOT];
-                const int32_t *il[NSLOT];
+            // Load order (the ring is a FIFO; the MMA thread and the release warps follow it):
+            //   round 0:  Q(s), K(s, 0) for each slot s
+            //   round r, tile t, slot s:  V(s, t), then K(s, t + 1) -- or, at t = K - 1, the next
+            //   round's Q(s) and K(s, 0), so the next unit's first QK can follow PV(s, K - 1) at once
+            int hh[NSLOT], jv[NSLOT];
+            const int32_t *il[NSLOT];
+            auto load_q = [&](int s, int u) {
+                mbar_wait(Q_EMPTY(s), ((qe_bits >> s) & 1u) ^ 1u);
+                qe_bits ^= 1u << s;
+                mbar_expect_tx(Q_FULL(s), B * D * 2);
+                if (TOK)
+                    tma_tile_tok<D / 64>(sQ + s * G::Q_BYTES, G::QCHUNK, tp.q, tp, u / NT, u - (u / NT) * NT, Q_FULL(s));
+                else
 #pragma unroll
-                for (int s = 0; s < NSLOT; ++s) {
-                    u[s] = UNIT_OF(r, s);
-                    act[s] = u[s] < total;
-                    hh[s] = act[s] ? u[s] / NT : 0;
-                    il[s] = p.idx + (size_t)(act[s] ? u[s] : 0) * K;
-                }
-#pragma unroll
-                for (int s = 0; s < NSLOT; ++s) {
-                    if (!act[s]) continue;
-                    mbar_wait(Q_EMPTY(s), ((qe_bits >> s) & 1u) ^ 1u);
-                    qe_bits ^= 1u << s;
-                    mbar_expect_tx(Q_FULL(s), B * D * 2);
-#pragma unroll
-                    if (TOK)
-                        tma_tile_tok<D / 64>(sQ + s * G::Q_BYTES, G::QCHUNK, tp.q, tp, hh[s], u[s] - hh[s] * NT,
-                                             Q_FULL(s));
-                    else
-                        for (int c = 0; c < D / 64; ++c)
-                            tma_load_2d(sQ + s * G::Q_BYTES + c * G::QCHUNK, &tmQ, c * 64, u[s] * B, Q_FULL(s));
-                }
-                auto load_tile = [&](const CUtensorMap *tm, int h, int j) {
-                    mbar_wait(RING_EMPTY(stage), ph ^ 1);
+                    for (int c = 0; c < D / 64; ++c)
+                        tma_load_2d(sQ + s * G::Q_BYTES + c * G::QCHUNK, &tmQ, c * 64, u * B, Q_FULL(s));
+            };
+            auto load_tile = [&](const CUtensorMap *tm, int h, int j) {
+                mbar_wait(RING_EMPTY(stage), ph ^ 1);
 #ifdef VEDA_DBG_SKIP_V  // timing experiment only: V tiles are not loaded (wrong results)
-                    if (tm == &tmV) {
-                        mbar_expect_tx(RING_FULL(stage), 0);
-                        if (++stage == G::NST) { stage = 0; ph ^= 1; }
-                        return;
-                    }
-#endif
-                    mbar_expect_tx(RING_FULL(stage), G::TILE_BYTES);
-                    const int row = (h * NT + j) * B;
-                    if (TOK)
-                        tma_tile_tok<D / 64>(sRing + stage * G::TILE_BYTES, G::KCHUNK, tm == &tmK ? tp.k : tp.v, tp,
-                                             h, j, RING_FULL(stage));
-                    else
-#pragma unroll
-                        for (int c = 0; c < D / 64; ++c)
-                            tma_load_2d(sRing + stage * G::TILE_BYTES + c * G::KCHUNK, tm, c * 64, row,
-                                        RING_FULL(stage));
+                if (tm == &tmV) {
+                    mbar_expect_tx(RING_FULL(stage), 0);
                     if (++stage == G::NST) { stage = 0; ph ^= 1; }
-                };
+                    return;
+                }
+#endif
+                mbar_expect_tx(RING_FULL(stage), G::TILE_BYTES);
+                const int row = (h * NT + j) * B;
+                if (TOK)
+                    tma_tile_tok<D / 64>(sRing + stage * G::TILE_BYTES, G::KCHUNK, tm == &tmK ? tp.k : tp.v, tp,
+                                         h, j, RING_FULL(stage));
+                else
 #pragma unroll
-                for (int s = 0; s < NSLOT; ++s)
-                    if (act[s]) { jv[s] = clamp_tile(__ldg(il[s]), NT); load_tile(&tmK, hh[s], jv[s]); }
-                for (int t = 0; t < K; ++t) {
+                    for (int c = 0; c < D / 64; ++c)
+                        tma_load_2d(sRing + stage * G::TILE_BYTES + c * G::KCHUNK, tm, c * 64, row,
+                                    RING_FULL(stage));
+                if (++stage == G::NST) { stage = 0; ph ^= 1; }
+            };
+            // unit u's index list, head and first K tile into the slot's registers
+            auto start_unit = [&](int s, int u) {
+                hh[s] = u / NT;
+                il[s] = p.idx + (size_t)u * K;
+                jv[s] = clamp_tile(__ldg(il[s]), NT);
+            };
+            // r = -1 is round 0's prologue (Q and first K only); one call site per load kind
+            // keeps the producer's code small (the token-layout TMA issue is long)
+            for (int r = -1; r < rounds; ++r) {
+                for (int t = (r < 0 ? K - 1 : 0); t < K; ++t) {
 #pragma unroll
                     for (int s = 0; s < NSLOT; ++s) {
-                        if (!act[s]) continue;
-                        const int jn = (t + 1 < K) ? clamp_tile(__ldg(il[s] + t + 1), NT) : 0;
-                        load_tile(&tmV, hh[s], jv[s]);
-                        if (t + 1 < K) { jv[s] = jn; load_tile(&tmK, hh[s], jv[s]); }
+                        if (r >= 0) {
+                            if (UNIT_OF(r, s) >= total) continue;
+                            load_tile(&tmV, hh[s], jv[s]);
+                        }
+                        if (t + 1 < K) {
+                            jv[s] = clamp_tile(__ldg(il[s] + t + 1), NT);
+                        } else {
+                            if (UNIT_OF(r + 1, s) >= total) continue;
+                            load_q(s, UNIT_OF(r + 1, s));
+                            start_unit(s, UNIT_OF(r + 1, s));
+                        }
+                        load_tile(&tmK, hh[s], jv[s]);
                     }
                 }
             }
@@ -211,13 +217,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) {
             const int s = warp - 2;
             uint32_t sf_ph = 0, of_ph = 0;
+            // global load index of K(s, t) / V(s, t) in the producer's order (see there)
+            uint32_t base = (UNIT_OF(0, 1) < total) ? 2 : 1;  // after round 0's first K tiles
+            uint32_t gk0 = s;                                  // K(s, 0) of the current round
             for (int r = 0; r < rounds; ++r) {
                 if (UNIT_OF(r, s) >= total) break;
                 const int A = (UNIT_OF(r, 1) < total) ? 2 : 1;
-                const uint32_t base = (uint32_t)r * (2 * NSLOT) * (uint32_t)K;
-                // global load index of K(s,t) / V(s,t) in the producer's order
-                auto gk = [&](int t) -> uint32_t { return base + (t == 0 ? s : A + 2 * A * (t - 1) + 2 * s + 1); };
-                auto gv = [&](int t) -> uint32_t { return base + A + 2 * A * t + ((t < K - 1) ? 2 * s : s); };
+                const int An = (UNIT_OF(r + 1, 0) < total) ? ((UNIT_OF(r + 1, 1) < total) ? 2 : 1) : 0;
+                const uint32_t tail = base + 2 * A * (K - 1);  // first load of tile K - 1
+                auto gk = [&](int t) -> uint32_t { return t == 0 ? gk0 : base + 2 * A * (t - 1) + 2 * s + 1; };
+                auto gv = [&](int t) -> uint32_t {
+                    return t < K - 1 ? base + 2 * A * t + 2 * s : tail + s + (s < An ? s : An);
+                };
                 for (int t = 0; t < K; ++t) {
                     mbar_wait(S_FULL(s), sf_ph);
                     sf_ph ^= 1;
@@ -227,6 +238,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mbar_wait(O_FULL(s), of_ph);
                 of_ph ^= 1;
                 mbar_arrive(RING_EMPTY(gv(K - 1) % G::NST));
+                gk0 = gv(K - 1) + 1;
+                base = tail + A + An;
             }
         }
         __syncwarp();
@@ -278,41 +291,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 if (t == K - 1 && hf == G::NPH - 1) tc_commit_w(O_FULL(s));
             };
+            // round 0's first QKs; every later unit's first QK follows its slot's last PV
+            for (int s = 0; s < NSLOT; ++s) {
+                if (UNIT_OF(0, s) >= total) continue;
+                uint32_t st, sp;
+                next_stage(st, sp);
+                mbar_wait(Q_FULL(s), (qf_bits >> s) & 1u);
+                qf_bits ^= 1u << s;
+                mbar_wait(RING_FULL(st), sp);
+                TR(0, nqk, 0);
+                tc_fence_after();
+                issue_qk(s, 0, st);
+                TR(0, nqk, 2);
+                ++nqk;
+            }
             for (int r = 0; r < rounds; ++r) {
-                uint32_t act_bits = 0;
-#pragma unroll
-                for (int s = 0; s < NSLOT; ++s) act_bits |= (UNIT_OF(r, s) < total ? 1u : 0u) << s;
-                for (int s = 0; s < NSLOT; ++s) {
-                    if (!((act_bits >> s) & 1u)) continue;
-                    uint32_t st, sp;
-                    next_stage(st, sp);
-                    mbar_wait(Q_FULL(s), (qf_bits >> s) & 1u);
-                    qf_bits ^= 1u << s;
-                    mbar_wait(RING_FULL(st), sp);
-                    TR(0, nqk, 0);
-                    tc_fence_after();
-                    issue_qk(s, 0, st);
-                    TR(0, nqk, 2);
-                    ++nqk;
-                }
                 for (int t = 0; t < K; ++t) {
                     for (int s = 0; s < NSLOT; ++s) {
-                        if (!((act_bits >> s) & 1u)) continue;
-                        const bool more = t + 1 < K;
+                        if (UNIT_OF(r, s) >= total) continue;
+                        const bool more = t + 1 < K, next = !more && UNIT_OF(r + 1, s) < total;
                         uint32_t sv, vp, sk = 0, kp = 0;
                         next_stage(sv, vp);
-                        if (more) next_stage(sk, kp);
+                        if (more || next) next_stage(sk, kp);
                         const uint32_t pp = (pf_bits >> s) & 1u;
                         pf_bits ^= 1u << s;
                         TR(0, npv, 3);
                         // non-blocking probe of the group's barriers (test_wait: an incomplete
                         // P_FULL must not put the thread to sleep), then wait for the rest
                         const uint32_t ok = mbar_try_wait4(P_FULL(s, 0), pp, RING_FULL(sv), vp,
-                                                           RING_FULL(more ? sk : sv), more ? kp : vp,
+                                                           RING_FULL((more || next) ? sk : sv), (more || next) ? kp : vp,
                                                            RING_FULL(sv), vp);
                         if (!(ok & 1u)) mbar_wait(P_FULL(s, 0), pp);
                         if (!(ok & 2u)) mbar_wait(RING_FULL(sv), vp);
-                        if (more && !(ok & 4u)) mbar_wait(RING_FULL(sk), kp);
+                        if ((more || next) && !(ok & 4u)) mbar_wait(RING_FULL(sk), kp);
                         TR(0, npv, 4);
                         tc_fence_after();
                         // P arrives in two halves: the first half's PV runs while the softmax
@@ -324,7 +335,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             tc_fence_after();
                             issue_pv(s, t, sv, 1);
                         }
-                        if (more) issue_qk(s, t + 1, sk);
+                        if (more) {
+                            issue_qk(s, t + 1, sk);
+                        } else if (next) {  // the slot's next unit: its S is ready by the end of the epilogue
+                            mbar_wait(Q_FULL(s), (qf_bits >> s) & 1u);
+                            qf_bits ^= 1u << s;
+                            tc_fence_after();
+                            issue_qk(s, 0, sk);
+                            ++nqk;
+                        }
                         TR(0, npv, 5);
                         ++npv;
                     }
