@@ -21,7 +21,7 @@
  *     no pointer after returning.  Host arrays are read during the call only.  The
  *     caller owns every buffer (workspace sizes come from the *_workspace helpers).
  *     Exceptions, all one-time or bounded: the first scoring call on a device uploads
- *     a 24 KB constant table (Phi for the GELU) into the library's static device
+ *     a 12 KB constant table (Phi for the GELU) into the library's static device
  *     memory and synchronises `stream` once; veda_sparse_attention_host creates two
  *     side streams per device on first use and a few events per call;
  *     veda_tile_select_pooled with several head chunks runs its top-k on one library side

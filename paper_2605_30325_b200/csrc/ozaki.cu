@@ -93,23 +93,24 @@ struct Img {
 };
 
 // GELU(x) = x Phi(x) (erf form, reading R8) in fp64 without the libdevice erf (which costs
-// ~70 FP64 instructions and made the layer-2 split FP64-bound): Phi on [-8, 8] from a
-// table of degree-4 Taylor polynomials around the centres of 768 intervals of width 1/48
-// (truncation <= (1/96)^5/120 max|Phi^(5)| ~ 1.2e-12 absolute, below the 2^-35 digit
-// quantum of a row); per interval 32 bytes = two 16-byte shared-memory loads (the split is
-// bound by these loads): c0, c1, c2 in fp64 and c3, c4 in fp32 (h^3 (c3 + c4 h) < 1.2e-7,
-// so fp32 adds < 1e-14); coefficients from Phi(c) = erfc(-c/sqrt2)/2 and
-// Phi^(n+1)(c) = (-1)^n He_n(c) phi(c), built once on the host; |x| >= 8: Phi = 0 or 1
-// (error < 7e-16).
+// ~70 FP64 instructions and made the layer-2 split FP64-bound): Phi on [-8, 8] by degree-4
+// Taylor polynomials around the centres c of 768 intervals of width 1/48 (truncation
+// <= (1/96)^5/120 max|Phi^(5)| ~ 1.2e-12 absolute, below the 2^-35 digit quantum of a row).
+// Every derivative of Phi is phi times a Hermite polynomial, Phi^(n+1)(c) = (-1)^n He_n(c)
+// phi(c), so an interval needs only {Phi(c), phi(c)} (16 bytes: ONE shared-memory load,
+// the split being bound by these loads) and
+//   Phi(c + h) = Phi(c) + phi(c) h (1 + h (-c/2 + h ((c^2-1)/6 - h (c^3-3c)/24)))
+// with the h^2 term in fp64 and the h^3, h^4 terms in fp32 (|h| <= 1/96: they are
+// < 2e-6 phi(c), so fp32 adds < 1e-13); table built once on the host from erfc / exp;
+// |x| >= 8: Phi = 0 or 1 (error < 7e-16).
 constexpr int PHI_N = 768;
 constexpr double PHI_SCALE = 48.0;        // intervals per unit of x: PHI_N = 16 * PHI_SCALE
 constexpr double PHI_W = 1.0 / 48.0;      // interval width (rounded); centre i: fma(i + 0.5, PHI_W, -8), host and device
 static_assert(PHI_N == 16 * 48, "Phi table layout");
 struct __align__(16) PhiEntry {
-    double c0, c1, c2;
-    float c3, c4;
+    double Phi, phi;  // Phi(c), phi(c) = exp(-c^2/2) / sqrt(2 pi)
 };
-static_assert(sizeof(PhiEntry) == 32, "two 16-byte loads per interval");
+static_assert(sizeof(PhiEntry) == 16, "one 16-byte load per interval");
 __device__ PhiEntry g_phi_tab[PHI_N];
 
 __device__ __forceinline__ double gelu_tab(double x, const PhiEntry *tab)
@@ -118,14 +119,14 @@ __device__ __forceinline__ double gelu_tab(double x, const PhiEntry *tab)
     if (x <= -8.0) return 0.0;
     int i = (int)((x + 8.0) * PHI_SCALE);
     if (i > PHI_N - 1) i = PHI_N - 1;
-    const double h = x - fma((double)i + 0.5, PHI_W, -8.0);  // no fp64 division
-    const uint4 *e = reinterpret_cast<const uint4 *>(tab + i);
-    const uint4 a = e[0], b = e[1];  // {c0, c1}, {c2, c3, c4}
-    const double c0 = __hiloint2double(a.y, a.x), c1 = __hiloint2double(a.w, a.z);
-    const double c2 = __hiloint2double(b.y, b.x);
-    const float t = fmaf(__uint_as_float(b.w), (float)h, __uint_as_float(b.z));  // c3 + c4 h
-    const double p = fma(fma(fma((double)t, h, c2), h, c1), h, c0);
-    return x * p;
+    const double c = fma((double)i + 0.5, PHI_W, -8.0);
+    const double h = x - c;  // no fp64 division
+    const uint4 a = *reinterpret_cast<const uint4 *>(tab + i);
+    const double P0 = __hiloint2double(a.y, a.x), p0 = __hiloint2double(a.w, a.z);
+    const float cf = (float)c, c2 = cf * cf, hf = (float)h;
+    const float t = fmaf(-cf * (c2 - 3.f) * (1.f / 24.f), hf, (c2 - 1.f) * (1.f / 6.f));
+    const double q = fma((double)t, h, -0.5 * c);
+    return x * fma(p0, h * fma(q, h, 1.0), P0);
 }
 
 // the same from the global table (L1-resident) -- used in the layer-1 GEMM epilogue, where
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(256, GELU ? 4 : 1) split_rows_kernel(const T *
     if (GELU) {
         const uint4 *g = reinterpret_cast<const uint4 *>(g_phi_tab);
         uint4 *d = reinterpret_cast<uint4 *>(s_tab);
-        for (int i = threadIdx.x; i < PHI_N * 2; i += 256) d[i] = g[i];
+        for (int i = threadIdx.x; i < PHI_N; i += 256) d[i] = g[i];
         __syncthreads();
     }
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, part = wi % WPR;
@@ -591,26 +592,11 @@ static veda_status phi_table_ready(cudaStream_t s)
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) dev = 0;
     if (done[dev].load(std::memory_order_acquire)) return VEDA_OK;
-    oz::PhiEntry tab[oz::PHI_N];  // 24 KB host staging; the upload below is synchronised before return
+    oz::PhiEntry tab[oz::PHI_N];  // 12 KB host staging; the upload below is synchronised before return
     const double inv_sqrt2pi = 0.39894228040143267794;
     for (int i = 0; i < oz::PHI_N; ++i) {
         const double c = std::fma((double)i + 0.5, oz::PHI_W, -8.0);  // the device's centre, bit for bit
-        const double phi = inv_sqrt2pi * std::exp(-0.5 * c * c);
-        double cf[5];
-        cf[0] = 0.5 * std::erfc(-c / std::sqrt(2.0));
-        // He_0 = 1, He_1 = c, He_{n+1} = c He_n - n He_{n-1};  coefficient of h^(n+1): (-1)^n He_n phi / (n+1)!
-        double he_prev = 1.0, he = c, fact = 1.0;
-        for (int n = 0; n < 4; ++n) {
-            const double hen = (n == 0) ? 1.0 : (n == 1 ? c : he);
-            fact *= (double)(n + 1);
-            cf[n + 1] = ((n & 1) ? -1.0 : 1.0) * hen * phi / fact;
-            if (n >= 1) {
-                const double next = c * he - (double)n * he_prev;
-                he_prev = he;
-                he = next;
-            }
-        }
-        tab[i] = oz::PhiEntry{cf[0], cf[1], cf[2], (float)cf[3], (float)cf[4]};
+        tab[i] = oz::PhiEntry{0.5 * std::erfc(-c / std::sqrt(2.0)), inv_sqrt2pi * std::exp(-0.5 * c * c)};
     }
     const cudaError_t e = cudaMemcpyToSymbolAsync(oz::g_phi_tab, tab, sizeof tab, 0, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return fail(VEDA_ERR_CUDA, "ozaki: Phi table upload: %s", cudaGetErrorString(e));
