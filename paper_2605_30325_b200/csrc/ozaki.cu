@@ -59,22 +59,39 @@ __device__ __forceinline__ int row_exponent(double m)
 // (|Y| <= 2^34, error <= 2^(e-35)); balanced base-128 digits are peeled off from the low
 // end, a_4 .. a_1 in [-64, 63], and a_0 = the rest (|a_0| <= 64), so
 // x ~ 2^e sum_s a_s 2^-(7s+6).  Digit s of value q goes to byte q of word s.
+// Peeling is a carry chain, Y_{j+1} = (Y_j + 64) >> 7, a_{4-j} = ((Y_j + 64) & 127) - 64,
+// whose closed form is offset binary: with C = 64 (128^5 - 1) / 127 and Z = Y + C >= 0,
+// a_{4-j} = bits [7j, 7j + 7) of Z minus 64 (j < 4) and a_0 = (Z >> 28) - 64.  Z comes from
+// ONE fma: x 2^(34-e) + (2^52 + C) lands in [2^52, 2^53), where the fp64 ulp is 1, so the
+// fma rounds x 2^(34-e) to the nearest integer (ties to even: 2^52 + C is even) exactly
+// like rint, and the low mantissa bits of the result are Z.  The four 7-bit fields of a
+// value are spread to the bytes of one word, the 4 x 4 bytes transposed with PRMTs, and
+// v - 64 taken per byte as the sign extension of the 7-bit v ^ 0x40.
 __device__ __forceinline__ void digits4(const double (&x)[4], int e, uint32_t (&w)[NS])
 {
+    static_assert(NS == 5, "digit layout");
     const double scale = __longlong_as_double((long long)(1023 + 34 - e) << 52);  // 2^(34-e)
-#pragma unroll
-    for (int s = 0; s < NS; ++s) w[s] = 0u;
+    constexpr double MAGIC = 4503599627370496.0 + 17315143744.0;                  // 2^52 + C
+    uint32_t sp[4], a0[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        long long Y = __double2ll_rn(x[q] * scale);
-#pragma unroll
-        for (int s = NS - 1; s > 0; --s) {
-            const int d = (int)((Y + 64) & 127) - 64;
-            Y = (Y - d) >> 7;
-            w[s] |= (uint32_t)(uint8_t)(int8_t)d << (8 * q);
-        }
-        w[0] |= (uint32_t)(uint8_t)(int8_t)(int)Y << (8 * q);
+        const double t = fma(x[q], scale, MAGIC);
+        const uint32_t lo = (uint32_t)__double2loint(t), hi = (uint32_t)__double2hiint(t);
+        a0[q] = __funnelshift_r(lo, hi, 28) - 64u;  // byte 0: a_0 (Z < 2^36: bits 28..35)
+        sp[q] = (lo & 0x7Fu) | ((lo << 1) & 0x7F00u) | ((lo << 2) & 0x7F0000u) | ((lo << 3) & 0x7F000000u);
     }
+    const uint32_t l01 = __byte_perm(sp[0], sp[1], 0x5140), h01 = __byte_perm(sp[0], sp[1], 0x7362);
+    const uint32_t l23 = __byte_perm(sp[2], sp[3], 0x5140), h23 = __byte_perm(sp[2], sp[3], 0x7362);
+    w[4] = __byte_perm(l01, l23, 0x5410);  // field 0 of values 0..3
+    w[3] = __byte_perm(l01, l23, 0x7632);
+    w[2] = __byte_perm(h01, h23, 0x5410);
+    w[1] = __byte_perm(h01, h23, 0x7632);
+#pragma unroll
+    for (int s = 1; s < NS; ++s) {
+        const uint32_t u = w[s] ^ 0x40404040u;
+        w[s] = u | ((u & 0x40404040u) << 1);
+    }
+    w[0] = __byte_perm(__byte_perm(a0[0], a0[1], 0x0040), __byte_perm(a0[2], a0[3], 0x0040), 0x5410);
 }
 
 // Digit images: the split kernels write each operand pre-tiled in exactly the shared-memory
