@@ -304,75 +304,86 @@ constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 // Epilogue of one 128 x BN output tile, run by the EPI_WARPS epilogue warps: stage the
 // per-column data, wait for the tile's accumulators (done_bar), read this warp's column
 // half from TMEM (releasing TMEM through tfree_bar once all of it is in registers),
-// combine the 5 accumulators exactly, scale, apply the epilogue op and store.
+// combine the 5 accumulators exactly, scale, apply the epilogue op and store.  The TMEM
+// reads use the 16x256b shape: lane t holds rows rbase + t/4 + {0, 8, 16, 24} and columns
+// 2(t%4) + {0, 1} and 8 + 2(t%4) + {0, 1} of each 16-column chunk, so four neighbouring
+// threads store 8 consecutive outputs of a row (64 B of fp64) -- a warp store touches 8
+// rows instead of 32 (the 32x32b row-per-thread form made every store 32 separate
+// L1 wavefronts, which competed with the tensor core's shared-memory operand reads).
 template <int BN, int EPI>
 __device__ __forceinline__ void epi_tile(const GemmArgs &g, uint32_t tl, int b, int m0, int n0, int cbeg, int cend,
-                                         int row, int ea, uint32_t done_bar, uint32_t done_parity, uint32_t tfree_bar,
-                                         const int *s_eb, const double *s_col)
+                                         int rbase, const int (&ea)[4], uint32_t done_bar, uint32_t done_parity,
+                                         uint32_t tfree_bar, const int *s_eb, const double *s_col)
 {
     // s_eb / s_col: this tile's per-column data (exponent of B's row, bias / score factor),
-    // staged in shared memory by the caller one tile ahead; ea: this row's A exponent
-    const int m = m0 + row;
-    const bool mok = m < g.M;
+    // staged in shared memory by the caller one tile ahead; ea: the A exponents of this
+    // thread's four rows rbase + t/4 + 8i
+    const int lane = threadIdx.x & 31, tr = lane >> 2, tc = 2 * (lane & 3);
+    const bool vec = (g.N % 2) == 0;  // 2-element vector stores stay aligned
     mbar_wait(done_bar, done_parity);
     tc_fence_after();
-    const int64_t orow = ((int64_t)b * g.M + m) * g.N;
 #pragma unroll 1
     for (int c0 = cbeg; c0 < cend; c0 += 16) {
-        uint32_t acc[NS][16];
+        uint32_t acc[NS][2][8];  // [accumulator][lane half: rows +0 / +16][register]
 #pragma unroll
-        for (int u = 0; u < NS; ++u) tmem_ld16(tl + (uint32_t)(u * BN + c0), acc[u]);
+        for (int u = 0; u < NS; ++u)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) tmem_ld16x256b_x2(tl + ((uint32_t)(16 * h) << 16) + (uint32_t)(u * BN + c0), acc[u][h]);
         tmem_wait_ld();
         if (c0 + 16 >= cend) {  // this warp's accumulator columns are in registers
             tc_fence_before();
             mbar_arrive(tfree_bar);
         }
-        if (!mok) continue;
-        // vector stores only when the whole 16-column run is in range and aligned
-        const bool full = n0 + c0 + 16 <= g.N && (g.N % 4) == 0;
-        double out[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            // sum_u acc_u 2^-(7u+12) = 2^-40 * sum_u acc_u 2^(7(4-u)): |acc_u| < 2^24, so
-            // the weighted sum is an exact int64 below 2^53 and converts to fp64 exactly
-            int64_t iv = 0;
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int u = 0; u < NS; ++u) iv += (int64_t)(int32_t)acc[u][i] << (7 * (NS - 1 - u));
-            const int sc = ea + s_eb[c0 + i] - (7 * (NS - 1) + 12) + 1023;  // biased exponent
-            const double v = (double)iv * __longlong_as_double((long long)sc << 52);
-            if (EPI == EPI_SCORE) {
-                const double f = s_col[c0 + i];  // 1/sqrt(d'), or -inf for an empty key tile
-                out[i] = (f == -INFINITY) ? -INFINITY : v * f;
-            } else if (EPI == EPI_GELU) {
-                out[i] = gelu_tab_g(v + s_col[c0 + i]);  // hidden = GELU(z W1 + b1)
-            } else {
-                out[i] = v + s_col[c0 + i];  // + bias
+            for (int rs = 0; rs < 2; ++rs) {  // row rbase + 16h + 8rs + t/4
+                const int m = m0 + rbase + 16 * h + 8 * rs + tr;
+                if (m >= g.M) continue;
+                const int64_t orow = ((int64_t)b * g.M + m) * g.N;
+#pragma unroll
+                for (int cb = 0; cb < 2; ++cb) {  // columns c0 + 8cb + 2(t%4) + {0, 1}
+                    const int cl = c0 + 8 * cb + tc;
+                    double o2[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int j = 4 * cb + 2 * rs + e;
+                        // sum_u acc_u 2^-(7u+12) = 2^-40 * sum_u acc_u 2^(7(4-u)): |acc_u| < 2^24, so
+                        // the weighted sum is an exact int64 below 2^53 and converts to fp64 exactly
+                        int64_t iv = 0;
+#pragma unroll
+                        for (int u = 0; u < NS; ++u) iv += (int64_t)(int32_t)acc[u][h][j] << (7 * (NS - 1 - u));
+                        const int sc = ea[2 * h + rs] + s_eb[cl + e] - (7 * (NS - 1) + 12) + 1023;  // biased exponent
+                        const double v = (double)iv * __longlong_as_double((long long)sc << 52);
+                        if (EPI == EPI_SCORE) {
+                            const double f = s_col[cl + e];  // 1/sqrt(d'), or -inf for an empty key tile
+                            o2[e] = (f == -INFINITY) ? -INFINITY : v * f;
+                        } else if (EPI == EPI_GELU) {
+                            o2[e] = gelu_tab_g(v + s_col[cl + e]);  // hidden = GELU(z W1 + b1)
+                        } else {
+                            o2[e] = v + s_col[cl + e];  // + bias
+                        }
+                    }
+                    const int n = n0 + cl;
+                    if (EPI == EPI_SCORE) {
+                        float *dst = static_cast<float *>(g.C) + orow + n;
+                        if (vec && n + 2 <= g.N)
+                            *reinterpret_cast<float2 *>(dst) = make_float2((float)o2[0], (float)o2[1]);
+                        else {
+                            if (n < g.N) dst[0] = (float)o2[0];
+                            if (n + 1 < g.N) dst[1] = (float)o2[1];
+                        }
+                    } else {
+                        double *dst = static_cast<double *>(g.C) + orow + n;
+                        if (vec && n + 2 <= g.N)
+                            *reinterpret_cast<double2 *>(dst) = make_double2(o2[0], o2[1]);
+                        else {
+                            if (n < g.N) dst[0] = o2[0];
+                            if (n + 1 < g.N) dst[1] = o2[1];
+                        }
+                    }
+                }
             }
-        }
-        if (EPI == EPI_SCORE) {
-            float *dst = static_cast<float *>(g.C) + orow + n0 + c0;
-            if (full) {
-#pragma unroll
-                for (int i = 0; i < 16; i += 4)
-                    *reinterpret_cast<float4 *>(dst + i) =
-                        make_float4((float)out[i], (float)out[i + 1], (float)out[i + 2], (float)out[i + 3]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (n0 + c0 + i < g.N) dst[i] = (float)out[i];
-            }
-        } else {
-            double *dst = static_cast<double *>(g.C) + orow + n0 + c0;
-            if (full) {
-#pragma unroll
-                for (int i = 0; i < 16; i += 2)
-                    *reinterpret_cast<double2 *>(dst + i) = make_double2(out[i], out[i + 1]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (n0 + c0 + i < g.N) dst[i] = out[i];
-            }
-        }
     }
 }
 
@@ -470,13 +481,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const int8_t *
     } else {  // ---- epilogue warps 2-9
         const int q = warp & 3;  // TMEM lane quarter (rows 32q .. 32q+31)
         const int cbeg = ((warp - 2) >> 2) * (BN / 2), cend = cbeg + BN / 2;  // this warp's column half
-        const int row = q * 32 + lane;
+        const int rbase = q * 32, tr = lane >> 2;  // this thread's rows: rbase + tr + 8i (16x256b reads)
         const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
         // per-column (and per-row) data of a tile is loaded into registers one tile ahead, so
         // its global-load latency overlaps the previous tile's epilogue; staged to shared
         // memory (double-buffered) behind one named barrier per tile
         const int tid = threadIdx.x - 64;
-        int eb_r = 0, ea_r = 0;
+        int eb_r = 0, ea_r[4] = {0, 0, 0, 0};
         double col_r = 0.0;
         auto load_cols = [&](int t) {
             int b, m0, n0;
@@ -490,7 +501,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const int8_t *
                 else
                     col_r = ok ? (double)__ldg(g.bias + (int64_t)b * g.N + n) : 0.0;
             }
-            ea_r = (m0 + row < g.M) ? __ldg(g.ea + (int64_t)b * g.M + m0 + row) : 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int m = m0 + rbase + tr + 8 * i;
+                ea_r[i] = (m < g.M) ? __ldg(g.ea + (int64_t)b * g.M + m) : 0;
+            }
         };
         if (blockIdx.x < ntiles) load_cols(blockIdx.x);
         int nt = 0;
@@ -502,10 +517,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) oz_gemm_kernel(const int8_t *
                 s_eb[buf][tid] = eb_r;
                 s_col[buf][tid] = col_r;
             }
-            const int ea = ea_r;
+            const int ea[4] = {ea_r[0], ea_r[1], ea_r[2], ea_r[3]};
             asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
             if (t + (int)gridDim.x < ntiles) load_cols(t + gridDim.x);
-            epi_tile<BN, EPI>(g, tl, b, m0, n0, cbeg, cend, row, ea, OZ_DONE, (uint32_t)nt & 1u, OZ_TFREE,
+            epi_tile<BN, EPI>(g, tl, b, m0, n0, cbeg, cend, rbase, ea, OZ_DONE, (uint32_t)nt & 1u, OZ_TFREE,
                               s_eb[buf], s_col[buf]);
         }
     }

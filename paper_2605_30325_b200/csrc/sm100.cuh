@@ -510,6 +510,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
+// 16 lanes x 16 consecutive 32-bit columns (16x256b.x2) -> 8 registers per thread.  Thread t
+// gets lane t/4 (r0, r1, r4, r5) and lane t/4 + 8 (r2, r3, r6, r7), columns 2(t%4) + {0, 1}
+// (r0-r3) and 8 + 2(t%4) + {0, 1} (r4-r7): four threads hold 8 consecutive columns of a lane
+// (layout measured on the B200: tools/micro/tmem_shape.cu)
+__device__ __forceinline__ void tmem_ld16x256b_x2(uint32_t taddr, uint32_t (&r)[8])
+{
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
 
 // Instruction descriptor, kind::f16: bf16 A/B, fp32 D.
 //  [4,6) D fmt (1 = f32) | [7,10) A fmt (1 = bf16) | [10,13) B fmt (1 = bf16)
