@@ -232,6 +232,39 @@ def test_dense_k_equals_nt(V, oracle, name):
     check_attention(oracle, u16(qt), u16(kt), u16(vt), idx.cpu().numpy(), bits32(mask), u16(o_t), tag=f"dense {name}")
 
 
+@pytest.mark.parametrize("name", ["toy_b128", "toy_b64_d128"])
+@pytest.mark.parametrize("pattern", ["half0", "half1", "huge", "ramp"])
+def test_online_softmax_rescale_paths(V, oracle, name, pattern):
+    """Online softmax (Eq. 2; A.1 renormalisation 545-551) when a later kept
+    tile raises the running row max: by > 8 (log2) in its first or second 64-key half (the
+    kernel's lazy rescale, detected before or after P half 0 went to the MMA), by > 128 (exps
+    against the stale reference overflow to inf and must be redone), and step by step along the
+    list.  Dense lists (k = N_T, ascending) so every query tile meets the scaled key tiles."""
+    c = Case(name, **CASES[name])
+    dev = torch.device("cuda")
+    qt, cnt, mask = V.tile_permute(c.q.to(dev), c.lat, c.cfgs)
+    kt, _, _ = V.tile_permute(c.k.to(dev), c.lat, c.cfgs, meta=False)
+    vt, _, _ = V.tile_permute(c.v.to(dev), c.lat, c.cfgs, meta=False)
+    Hh, NT, B = qt.shape[:3]
+    j = NT // 2
+    hi = slice(B // 2, B) if B == 128 else slice(0, B)
+    if pattern == "half0":
+        kt[:, j, : min(64, B)] *= 6
+    elif pattern == "half1":
+        kt[:, j, hi] *= 6
+    elif pattern == "huge":
+        kt[:, 1, : min(64, B)] *= 4
+        kt[:, j, hi] *= 60
+    else:
+        for t in range(1, NT):
+            kt[:, t] *= 1.0 + 0.25 * t
+    idx = torch.arange(NT, dtype=torch.int32, device=dev).expand(Hh, NT, NT).contiguous()
+    o_t, lse = V.sparse_attn_fwd(qt, kt, vt, idx, mask, want_lse=True)
+    assert torch.isfinite(o_t.float()).all()
+    check_attention(oracle, u16(qt), u16(kt), u16(vt), idx.cpu().numpy(), bits32(mask), u16(o_t), lse.cpu().numpy(),
+                    tag=f"rescale {name} {pattern}")
+
+
 @pytest.mark.parametrize("kk", [1, 3])
 def test_random_lists_and_small_k(V, oracle, kk):
     """Regime R2 (uniformly random kept lists) and k = 1 edge case."""
