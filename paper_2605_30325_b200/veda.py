@@ -647,6 +647,22 @@ class SparseAttention:
         return (tile_permute(q, lat, cfgs, meta=False)[0], tile_permute(k, lat, cfgs, meta=False)[0],
                 tile_permute(v, lat, cfgs, meta=False)[0])
 
+    def capture(self, q, k, v, out):
+        """Record one call on (q, k, v, out) into a CUDA graph and return it
+        (``g.replay()`` re-runs every kernel of the call on those same buffers; the fused
+        select's side-stream fork / join is captured with it).  Removes the per-call launch
+        gaps: measured ~0.1 ms on the score + top-k step at Waver (tools/graph_bench.py).
+        The library must already be warm on this device (one eager call first: the Phi
+        table upload is synchronous)."""
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=q.device)
+        s.wait_stream(torch.cuda.current_stream(q.device))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+                self(q, k, v, out=out)
+        torch.cuda.current_stream(q.device).wait_stream(s)
+        return g
+
     def __call__(self, q, k, v, out=None, events=None):
         """Run the path; ``events`` (optional list of 6 torch.cuda.Event) brackets the steps."""
         lib, s = load(), _stream()
