@@ -106,7 +106,7 @@ def main():
     with open(a.out + ".md", "w") as f:
         gs = [G for G in SHARDS if rows and f"rank_ms_G{G}" in rows[0]]
         f.write("| workload | tokens | heads | N_T | sparsity | k | call ms | attn ms | attn TFLOP/s | dense attn ms | "
-                "dense TFLOP/s | call speedup vs dense |" + "".join(f" busiest rank, G={G} (ms) |" for G in gs) +
+                "dense TFLOP/s | call speedup vs dense |" + "".join(f" busiest rank, G={G} (ms, 1-GPU proxy) |" for G in gs) +
                 "\n|---|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|" + "---:|" * len(gs) + "\n")
         for r in rows:
             f.write(f"| {r['workload']} | {r['tokens']} | {r['heads']} | {r['n_tiles']} | {r['sparsity']:.2f} | "
