@@ -112,7 +112,8 @@ __device__ __forceinline__ void tma_tile_tok(uint32_t dst, uint32_t stride, cons
 #define DBG(...) do { } while (0)
 #endif
 
-// Fraction of exp2 evaluated on the FMA pipe instead of MUFU: one pair in every
+// Experiments only (tools/experimental/*.cu; the product kernel uses MUFU for every exp):
+// fraction of exp2 evaluated on the FMA pipe instead of MUFU: one pair in every
 // EMU_EVERY (0 disables).  MUFU.EX2 runs at 16/clk/SM, the same rate at which the
 // tensor core consumes a 128x128 score tile.  Measured (profiles/r01_attn_experiments.md):
 // slower at the current balance (the MMA issue chain, not MUFU, is critical), so off.

@@ -159,13 +159,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             };
             auto load_tile = [&](const CUtensorMap *tm, int h, int j) {
                 mbar_wait(RING_EMPTY(stage), ph ^ 1);
-#ifdef VEDA_DBG_SKIP_V  // timing experiment only: V tiles are not loaded (wrong results)
-                if (tm == &tmV) {
-                    mbar_expect_tx(RING_FULL(stage), 0);
-                    if (++stage == G::NST) { stage = 0; ph ^= 1; }
-                    return;
-                }
-#endif
                 mbar_expect_tx(RING_FULL(stage), G::TILE_BYTES);
                 const int row = (h * NT + j) * B;
                 if (TOK)
@@ -441,13 +434,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const int c = 2 * c2 + (i >> 4), e = (i & 15) * 2;
                         float x0, x1;
                         ffma2_bc(x0, x1, u2f(sr[c][e]), u2f(sr[c][e + 1]), sl2, -mu);
-                        float a, b;
-                        if (EMU_EVERY > 0 && (i % EMU_EVERY) == EMU_EVERY - 1) {
-                            ex2_emu2(a, b, x0, x1);  // FMA-pipe polynomial: unloads the MUFU unit
-                        } else {
-                            a = ex2(x0);
-                            b = ex2(x1);
-                        }
+                        const float a = ex2(x0), b = ex2(x1);  // MUFU (FMA-pipe emulation measured slower)
                         fadd2_acc(ps[(i & 1) * 2], ps[(i & 1) * 2 + 1], a, b);
                         pk[i] = pack_bf16(a, b);
                     }
