@@ -1,5 +1,5 @@
 """Whole-call timings of the fp64 CPU oracle: every head and every
-query tile of the tiny and Wan2.1-1.3B workloads on this host's cores, plus a single-thread
+query tile of the tiny, Wan2.1-1.3B and (--wan14b) Wan2.1-14B workloads on this host's cores, plus a single-thread
 figure, next to the bounded Waver sample that bench.py's cpu_baseline uses.  A reported
 baseline, not a target.
 
@@ -19,6 +19,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--skip-wan", action="store_true")
+    ap.add_argument("--wan14b", action="store_true", help="also the whole Wan2.1-14B call (~3 min on 16 cores)")
     a = ap.parse_args()
     from paper_2605_30325_b200 import synth
 
@@ -28,6 +29,8 @@ def main():
     res["tiny_full_call_ms"] = round(bench.oracle_full("tiny"), 2)
     if not a.skip_wan:
         res["wan1.3b_full_call_ms"] = round(bench.oracle_full("wan1.3b"), 1)
+    if a.wan14b:
+        res["wan14b_full_call_ms"] = round(bench.oracle_full("wan14b"), 1)
     pre = synth.PRESETS["waver12b"]
     ms, cores, sample, wall, single = bench.oracle_sample(pre, pre.sparsity, 240, single_thread_units=8)
     res["waver12b_extrapolated_ms"] = round(ms, 1)
