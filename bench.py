@@ -507,6 +507,11 @@ def run_ours(args):
                        "parallelism": f"heads{world}", "l2": "inputs larger than L2 (no flush)",
                        "regime": "path-produced lists"},
             "speedup_vs_dense": round(dense_ms / ms_step, 2),
+            # SURVEY §8(d) d1's other two ratios: kernel / kernel (same attention kernel at k = N_T
+            # vs k), and path / path (the dense path of the token layout is that same kernel:
+            # no tiled copies to add, untiling fused), so it equals the headline here
+            "speedup_kernel_vs_kernel": round(dense_ms / attn_ms, 2),
+            "speedup_path_vs_path": round(dense_ms / ms_step, 2),
             "dense_kernel_ms": round(dense_ms, 2),
             "attn_kernel_ms": round(attn_ms, 3),
             "attn_kernel_ms_random_lists": round(rand_attn_ms, 3),
