@@ -125,6 +125,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def versions():
+    """Driver / CUDA / torch versions of the run."""
+    import torch
+
+    drv = None
+    try:
+        out = subprocess.run(["nvidia-smi", "--query-gpu=driver_version,name", "--format=csv,noheader"],
+                             capture_output=True, text=True, timeout=20).stdout.strip().splitlines()
+        drv = out[0] if out else None
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"driver_gpu": drv, "cuda_runtime": torch.version.cuda, "torch": torch.__version__}
+
+
 # ----------------------------------------------------------------------------- oracle timing
 def cpu_model():
     try:
@@ -557,6 +571,7 @@ def run_ours(args):
                                "source": "PAPER.md:471", "value_over_paper": round(ms_step / 309.1, 4)}
                               if args.workload == "waver12b" and abs(sp - 0.95) < 1e-9 else None),
             "clocks": clock,
+            "versions": versions(),
         }
         print(json.dumps(result), flush=True)
     if multi:
