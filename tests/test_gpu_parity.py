@@ -351,7 +351,7 @@ def test_end_to_end_path_object(V, oracle, mode):
     assert torch.equal(path(q, k, v), o)
 
 
-@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
 @pytest.mark.parametrize("uniform", [True, False])
 def test_path_object_unit_shares(V, G, uniform):
     """Rank shares of the whole path (SparseAttention(units=shard.unit_range(...)): pooling on
