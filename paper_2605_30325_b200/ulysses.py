@@ -90,6 +90,7 @@ def head_to_seq_async(o_heads: torch.Tensor, lat, heads_of, group=None):
             ov[:, hj.start:hj.stop, :] = recv[off:off + n].view(Nr, len(hj), dp)
             off += n
 
+    place.recv = recv  # callers that place on another stream record it there (record_stream)
     return place, work
 
 
@@ -170,22 +171,57 @@ class UlyssesSparseAttention:
                                                    head_range=hc))
         self.path = self.paths[0]
 
-    def __call__(self, q, k, v):
+    def __call__(self, q, k, v, trace=None):
+        """``trace`` (optional list): (label, torch.cuda.Event) pairs recorded on the current
+        stream -- start, each chunk's inputs usable / path done, the end -- for overlap
+        timelines (tools/ulysses_overlap.py).
+
+        Streams: the send buffers of every chunk are packed and their all-to-alls issued on a
+        side stream ``xs`` (in chunk order, so chunk 0 lands first); the caller's stream runs
+        chunk c's path as soon as chunk c's three exchanges are done; chunk c's output
+        exchange (pack + all-to-all) is issued on a second side stream ``xo`` once its path
+        is done; the received rows are placed into ``out`` on the caller's stream at the end."""
         C, G = self.chunks, self.world
+        cs = torch.cuda.current_stream(q.device)
+        if not hasattr(self, "_xs"):
+            self._xs, self._xo = torch.cuda.Stream(device=q.device), torch.cuda.Stream(device=q.device)
+        xs, xo = self._xs, self._xo
+
+        def mark(label):
+            if trace is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(cs)
+                trace.append((label, e))
+
+        mark("start")
         heads_of = [[chunk_range(head_range(self.Hh, j, G), c, C) for j in range(G)] for c in range(C)]
-        ins = [[seq_to_head_async(t, self.lat, heads_of[c], self.group) for t in (q, k, v)] for c in range(C)]
+        xs.wait_stream(cs)  # q, k, v are ready on the caller's stream
+        with torch.cuda.stream(xs):
+            ins = [[seq_to_head_async(t, self.lat, heads_of[c], self.group) for t in (q, k, v)] for c in range(C)]
+        for c in range(C):
+            for r, _ in ins[c]:
+                r.record_stream(cs)  # allocated on xs, read by the path on cs
+        mark("inputs issued")
         outs = []
         for c in range(C):
             for _, work in ins[c]:
-                work.wait()
+                work.wait()  # the caller's stream waits for chunk c's exchanges only
+            mark(f"chunk {c} inputs in")
             qh, kh, vh = (r for r, _ in ins[c])  # [N, h_c, d]
             o = torch.empty_like(qh)
             if qh.shape[1]:
                 # the path reads/writes [h_c, N, d] views of the [N, h_c, d] buffers (strided, no copy)
                 self.paths[c](qh.transpose(0, 1), kh.transpose(0, 1), vh.transpose(0, 1), out=o.transpose(0, 1))
-            outs.append(head_to_seq_async(o, self.lat, heads_of[c], self.group))
+            mark(f"chunk {c} path done")
+            xo.wait_stream(cs)
+            o.record_stream(xo)
+            with torch.cuda.stream(xo):
+                place, work = head_to_seq_async(o, self.lat, heads_of[c], self.group)
+            place.recv.record_stream(cs)  # allocated on xo, read by place() on cs
+            outs.append((place, work))
         out = torch.empty_like(q)
         for place, work in outs:
             work.wait()
             place(out)
+        mark("end")
         return out
