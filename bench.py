@@ -44,7 +44,6 @@ def parse():
     ap.add_argument("--dense-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing (context)")
     ap.add_argument("--host-chunk", type=int, default=0,
                     help="heads per chunk of the host pipeline (0 = library default, ceil(Hh/32))")
     ap.add_argument("--cpu-sample-units", type=int, default=720,
@@ -437,25 +436,6 @@ def run_ours(args):
         path._host_ws_key = None
         del qh, kh, vh, oh
 
-    # the same call recorded once as a CUDA graph (SparseAttention.capture) and replayed: the
-    # launch gaps removed; context next to the eager value (the headline stays the eager call)
-    graph_ms = None
-    if not args.no_graph:
-        try:
-            g = path.capture(q, k, v, out)
-            g.replay()
-            barrier()
-            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            g0.record(stream)
-            for _ in range(args.steps):
-                g.replay()
-            g1.record(stream)
-            barrier()
-            graph_ms = shard.max_over_ranks(g0.elapsed_time(g1) / args.steps)
-            del g
-        except Exception as exc:  # context only: never fail the bench line on it
-            print(f"bench: CUDA graph capture skipped: {exc}", file=sys.stderr)
-
     # optional Ulysses mode (N > 1): sequence-sharded inputs [N_r, Hh, d], all-to-all to
     # heads, local path, all-to-all back; its two exchanges are the only collectives
     ulysses_ms = None
@@ -563,7 +543,6 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": int(launches),
             "ulysses_ms_per_call": None if ulysses_ms is None else round(ulysses_ms, 3),
-            "graph_replay_ms_per_call": None if graph_ms is None else round(graph_ms, 3),
             # the paper's latency for the same token count (Waver 720P/241f, 245,760 padded tokens)
             # on Hopper with "SP=8" -- another machine and an
             # ambiguous GPU count, so context only (vs_baseline stays null)

@@ -9,7 +9,7 @@ TAG=${1:-final}
 WHAT=${2:-ncu}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${TAG}_build.log 2>&1 || { echo BUILD FAILED; tail -30 gpurun_out/${TAG}_build.log; exit 1; }
-B="python bench.py --steps 1 --warmup 1 --dense-steps 1 --no-cpu-baseline --no-e2e --no-graph"
+B="python bench.py --steps 1 --warmup 1 --dense-steps 1 --no-cpu-baseline --no-e2e"
 case "$WHAT" in
 ncu)
   # attention: one launch of the token-layout kernel at Waver / 24 heads (the bench's)

@@ -21,11 +21,11 @@ echo "bench exit $?"; cat gpurun_out/${TAG}_bench.json; tail -5 gpurun_out/${TAG
 if [ "$NCU" = ncu ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --dense-steps 1 \
-    --no-cpu-baseline --no-e2e --no-graph > gpurun_out/${TAG}_ncu_bench.log 2>&1
+    --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu_bench.log 2>&1
   echo "ncu launches exit $?"
   timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active,lts__t_sector_hit_rate.pct,sm__cycles_elapsed.avg.per_second \
     --clock-control none -k regex:sparse_attn_fwd -c 1 --csv --log-file gpurun_out/${TAG}_attn_metrics.csv \
-    python bench.py --steps 1 --warmup 0 --dense-steps 1 --no-cpu-baseline --no-e2e --no-graph > gpurun_out/${TAG}_ncu_attn.log 2>&1
+    python bench.py --steps 1 --warmup 0 --dense-steps 1 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu_attn.log 2>&1
   echo "ncu attention metrics exit $?"
 fi
 if [ "$CPU" = cpu ]; then
