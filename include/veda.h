@@ -324,7 +324,7 @@ VEDA_API veda_status veda_tile_score_pooled(const float *zq, const float *zk, co
  * kernel-level fusion to reduce mask preparation overhead"): the kept-tile lists idx
  * [Hh][N_T][k] straight from the pooled descriptors, with no [Hh][N_T][N_T] score tensor.
  * phi_q / phi_k (Eq. 6) run for all heads; then, per chunk of heads_per_chunk heads
- * (0: as many as fit 48 MB of fp32 scores -- 3 of Waver's 24), S_pred (Eq. 6) is written
+ * (0: as many as fit 128 MB of fp32 scores -- 8 of Waver's 24), S_pred (Eq. 6) is written
  * to a chunk-sized scratch in the workspace and the top-k of veda_select_topk
  * reads it back; with several chunks the scratch is double-
  * buffered and the top-k of chunk c runs on a library side stream while the score GEMM

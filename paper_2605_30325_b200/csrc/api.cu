@@ -383,14 +383,16 @@ veda_status veda_tile_score_pooled(const float *zq, const float *zk, const int32
 // Steps 2 (phi, S_pred) + 3 (top-k) without a [Hh][N_T][N_T] score tensor: phi_q / phi_k
 // and the digit images of e_q / e_k for all heads, then per chunk of heads the score GEMM
 // into a [chunk][N_T][N_T] scratch that the top-k reads back.  Default chunk: as many heads
-// as fit 48 MB of fp32 scores (3 of Waver's 24), double-buffered (88 MB instead of 354 MB),
+// as fit 128 MB of fp32 scores (8 of Waver's 24), double-buffered (236 MB instead of 354 MB),
 // the top-k of chunk c on a side stream beside the score GEMM of chunk c+1
-// (tools/select_bench.py at Waver: 1.71 ms vs 1.59 for the two-call form with the full S).
+// (tools/select_bench.py at Waver: 8-head chunks 1.41 ms, 3-head chunks 1.54-1.63, one chunk
+// = the two-call form with the full S 1.34-1.43: fewer, larger chunks waste less in the
+// persistent GEMM's last wave and in the chunk hand-offs).
 static int select_chunk_heads(int Hh, int NT, int heads_per_chunk)
 {
     if (heads_per_chunk > 0) return std::min(heads_per_chunk, Hh);
     const size_t per_head = (size_t)NT * NT * sizeof(float);
-    const size_t budget = (size_t)48 << 20;
+    const size_t budget = (size_t)128 << 20;
     return (int)std::max<size_t>(1, std::min<size_t>((size_t)Hh, budget / per_head));
 }
 

@@ -396,10 +396,10 @@ def tile_score_pooled(zq, zk, tile_count, scorer: Scorer, workspace: ScoreWorksp
 
 def select_chunk_heads(Hh: int, n_tiles: int, heads_per_chunk: int = 0) -> int:
     """Heads per score chunk of veda_tile_select_pooled (mirrors the library: as many heads
-    as fit 48 MB of fp32 scores, at least one, unless given)."""
+    as fit 128 MB of fp32 scores, at least one, unless given)."""
     if heads_per_chunk > 0:
         return min(heads_per_chunk, Hh)
-    return max(1, min(Hh, (48 << 20) // (n_tiles * n_tiles * 4)))
+    return max(1, min(Hh, (128 << 20) // (n_tiles * n_tiles * 4)))
 
 
 class SelectWorkspace:
